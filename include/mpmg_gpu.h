@@ -1,0 +1,228 @@
+/* mpmg_gpu.h — C ABI of the B200-native mixed-precision IR + geometric
+ * multigrid hot path (arxiv 2007.07539, BASELINE.json north_star).
+ *
+ * Two layers, both plain C (no torch or C++ types in any signature):
+ *
+ *  1. mpmg_gpu_*  — one entry point per fused sm_100a kernel family. Device
+ *     pointers, sizes, a precision code, a policy word and a cudaStream_t
+ *     (passed as void*). Asynchronous on the stream; never throws; returns
+ *     MPMG_OK or a negative MPMG_E* code. Scalars that are produced on the
+ *     device (alpha = ||r||, restriction scales) are passed as device pointers.
+ *     These replace the reference's kernel layer (core/include/mpmg/kernels.hpp
+ *     :11-38 and the level operations of multigrid.hpp:73-94); see each entry.
+ *
+ *  2. mpmg_solver_* — handle API over the whole hot path (hierarchy build,
+ *     V-cycle, IR solve) with HOST buffers, mirroring MgHierarchy::build
+ *     (multigrid.hpp:104-107), MgHierarchy::v_cycle (multigrid.hpp:119) and
+ *     ir_solve (ir_solver.hpp:57-60). This is what an FFI (ctypes/cgo/JNI)
+ *     binds; the C++ drop-in API (include/mpmg/*.hpp) is built on it.
+ *
+ * Device vector layout ("ghost-aliased pitch layout"). A level with n nodes
+ * per dimension (boundary included) has pitch P = n - 1 and stores node
+ * (x, y[, z]) with x, y, z in [0, P] at x + P*y (+ P*P*z). Node x = P of one
+ * row aliases node x = 0 of the next row; both are Dirichlet boundary nodes,
+ * stored as zero and never written, so the stencil needs no boundary
+ * branches. Allocation: P^3 + P^2 + P + 1 (3D) or P^2 + P + 1 (2D) values.
+ * The reference's compact interior ordering (mesh_fem.hpp:43-50, x fastest)
+ * converts with mpmg_gpu_pack / mpmg_gpu_unpack.
+ */
+#ifndef MPMG_GPU_H
+#define MPMG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Precision codes == mpmg::Precision (precision.hpp:12). */
+enum { MPMG_FP16 = 0, MPMG_FP32 = 1, MPMG_FP64 = 2 };
+
+/* Variant codes == mpmg::MgVariant (multigrid.hpp:19). */
+enum { MPMG_D_MG = 0, MPMG_H_MG = 1, MPMG_DSH_MG = 2, MPMG_HSD_MG = 3 };
+
+/* Policy word: ArithmeticPolicy (precision.hpp:32-35) + Fp16Accum
+ * (traffic.hpp:35). Reference default = MPMG_FTZ | MPMG_FMA. */
+enum { MPMG_FTZ = 1u, MPMG_FMA = 2u, MPMG_ACC32 = 4u };
+
+/* Return codes. */
+enum {
+  MPMG_OK = 0,
+  MPMG_EINVAL = -1,      /* std::invalid_argument in the reference */
+  MPMG_ENONFINITE = -2,  /* DivergedError / ValidationError */
+  MPMG_ECUDA = -3,       /* CUDA runtime failure */
+  MPMG_EBUILD = -4,      /* HierarchyBuildError (binary16 overflow) */
+  MPMG_ENOMEM = -5,
+  MPMG_EUNSUPPORTED = -6
+};
+
+/* One level's operator: the reference's per-level ELL matrix is a constant
+ * stencil (every row's slot value for a given offset is bitwise identical,
+ * SURVEY §8a-R0; checked against the reference in tests/test_hierarchy.py).
+ * taps are lexicographic (dz, dy, dx), already rounded to `prec`. */
+typedef struct mpmg_stencil {
+  int32_t dim;      /* 2 or 3 */
+  int32_t nodes;    /* nodes per dimension incl. boundary; pitch P = nodes-1 */
+  int32_t prec;     /* storage == arithmetic precision of this level */
+  int32_t ntaps;    /* 9 or 27 */
+  double taps[27];  /* value domain, rounded to prec */
+  double inv_diag;  /* Jacobi D^-1 (per-level constant), rounded to prec */
+} mpmg_stencil;
+
+/* Number of values of a padded level vector. */
+size_t mpmg_padded_len(int32_t dim, int32_t nodes);
+/* Number of interior unknowns ((n-2)^dim). */
+size_t mpmg_interior_len(int32_t dim, int32_t nodes);
+/* Bytes per value of a precision code (precision.hpp:14-20). */
+int mpmg_bytes_per_value(int32_t prec);
+
+/* Last CUDA error string of this thread (for diagnostics). */
+const char* mpmg_last_error(void);
+
+/* ---- layer 1: kernels (device pointers, padded layout) -------------------*/
+
+/* compact interior (reference ordering) <-> padded; ghosts written as zero */
+int mpmg_gpu_pack(int32_t dim, int32_t nodes, int32_t prec, const void* compact, void* padded, void* stream);
+int mpmg_gpu_unpack(int32_t dim, int32_t nodes, int32_t prec, const void* padded, void* compact, void* stream);
+
+/* One damped-Jacobi step u_out = u_in + w D^-1 (b - A u_in), every operation
+ * rounded to the level precision in the reference's order:
+ * jacobi_smooth multigrid.cpp:79-89 = spmv (kernels.cpp:137-193), axpy(-1)
+ * (:195-212), vec_multiply (:214-229), axpy(omega). u_in == NULL means the
+ * step starts from u = 0 (multigrid.cpp:376). u_in and u_out must differ. */
+int mpmg_gpu_jacobi(const mpmg_stencil* A, const void* b, const void* u_in, void* u_out, double omega,
+                    uint32_t policy, void* stream);
+
+/* Level defect r = b - A u in the level precision (multigrid.cpp:379-380). */
+int mpmg_gpu_defect(const mpmg_stencil* A, const void* b, const void* u, void* r, uint32_t policy, void* stream);
+
+/* y = A x in the level precision (kernels.cpp:137-193). */
+int mpmg_gpu_spmv(const mpmg_stencil* A, const void* x, void* y, uint32_t policy, void* stream);
+
+/* Full-weighting restriction with precision change (restrict_with_cast,
+ * multigrid.cpp:236-268): r_c = round_{coarse_prec}(R r_f / scale), the
+ * product accumulated in fine_prec with per-op rounding. `scale_dev` is a
+ * device double (NULL = 1.0). fine grid has `fine_nodes` nodes per dim. */
+int mpmg_gpu_restrict(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_t coarse_prec, const void* r_fine,
+                      void* r_coarse, const double* scale_dev, uint32_t policy, void* stream);
+
+/* Prolongation + correction (prolong_with_cast multigrid.cpp:270-280 and
+ * axpy(1) :389-390): u_f = round_f(u_f + round_f(scale * (P c_c))), P c_c in
+ * coarse_prec with per-op rounding. `scale_dev` device double (NULL = 1.0). */
+int mpmg_gpu_prolong_correct(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_t coarse_prec,
+                             const void* c_coarse, void* u_fine, const double* scale_dev, uint32_t policy,
+                             void* stream);
+
+/* Outer FP64 defect r = b - A u (ir_solver.cpp:92-93); when `partials` is
+ * non-NULL also writes per-block partial sums of r_i^2 for mpmg_gpu_norm_finalize. */
+int mpmg_gpu_defect_f64(const mpmg_stencil* A64, const double* b, const double* u, double* r, double* partials,
+                        void* stream);
+
+/* Fused update (update_residuum_correction kernels.cpp:300-341): u += a*c,
+ * r -= a * A c, all FP64 with c (precision c_prec) widened on read. `alpha_dev`
+ * is a device double. Optional norm partials of the new r. */
+int mpmg_gpu_update_rc(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, double* u,
+                       const double* alpha_dev, double* partials, uint32_t policy, void* stream);
+
+/* Scaled downcast (cast_vector kernels.cpp:343-360): out = round_prec(x / s)
+ * with s = *alpha_dev if (scale_enabled && *alpha_dev > 0) else 1. */
+int mpmg_gpu_scale_downcast(int32_t dim, int32_t nodes, const double* x, void* out, int32_t prec,
+                            const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream);
+
+/* Number of partial sums written by the partial-producing kernels. */
+int mpmg_gpu_partials_len(int32_t dim, int32_t nodes);
+/* Norm of a padded FP64 vector: deterministic two-stage reduction (fixed
+ * block partition, fixed-order final sum). Writes sqrt(sum) to *out_dev. */
+int mpmg_gpu_norm2_f64(int32_t dim, int32_t nodes, const double* x, double* partials, double* out_dev,
+                       void* stream);
+int mpmg_gpu_norm_finalize(const double* partials, int32_t n_partials, double* out_dev, void* stream);
+
+/* The per-level operator of MgHierarchy::build (multigrid.cpp:290-310) for a
+ * grid of `nodes` nodes per dimension in precision `prec`: the assembled Q1
+ * coefficients (mesh_fem.cpp:71-155) rounded per policy, and D^-1. Returns
+ * MPMG_EBUILD on binary16 overflow (cast_checked, multigrid.cpp:25-33). */
+int mpmg_build_stencil(int32_t dim, int32_t nodes, int32_t prec, uint32_t policy, mpmg_stencil* out);
+
+/* quantize_fp16 (precision.cpp:23-48) on the host. */
+double mpmg_round_fp16(double x, int32_t ftz);
+
+/* ---- layer 2: solver handle (host buffers) --------------------------------*/
+
+typedef struct mpmg_solver mpmg_solver;
+
+typedef struct mpmg_solver_config {
+  int32_t dim, k, nodes, levels, variant;
+  int32_t pre_steps, post_steps;  /* SmootherConfig (multigrid.hpp:31-35) */
+  double omega;
+  double base_tol;                /* BaseSolverConfig (multigrid.hpp:41-46) */
+  int32_t base_mode;              /* 0 RelativeToRhs, 1 Absolute */
+  int32_t base_max_iterations;    /* 0 = 10 x base unknowns */
+  uint32_t policy;                /* MPMG_FTZ | MPMG_FMA | MPMG_ACC32 */
+  int32_t device;
+} mpmg_solver_config;
+
+typedef struct mpmg_solve_params {   /* IrConfig (ir_solver.hpp:12-24) */
+  double outer_tolerance;            /* absolute ||r||_2 bound */
+  int32_t max_outer_iterations;
+  int32_t random_initial_guess;      /* InitialGuess::SeededRandom01 */
+  uint64_t seed;
+  int32_t scaling;                   /* 0 VariantDefault, 1 ForceOn, 2 ForceOff */
+  int32_t residual_refresh_interval;
+  int32_t use_graph;                 /* capture the loop as one CUDA graph */
+} mpmg_solve_params;
+
+typedef struct mpmg_solve_report {   /* SolveReport (ir_solver.hpp:26-44) */
+  int32_t converged;
+  int32_t iterations;
+  double final_residual;
+  double device_seconds;             /* CUDA-event time of the solve */
+  double wall_seconds;
+} mpmg_solve_report;
+
+void mpmg_solver_default_config(mpmg_solver_config* cfg);
+void mpmg_solve_default_params(mpmg_solve_params* p);
+
+/* Builds the device-resident hierarchy (MgHierarchy::build semantics) and
+ * the FP64 finest operator. Returns NULL on error; *err receives the code and
+ * *err_level the offending level for MPMG_EBUILD. */
+mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* err_level);
+void mpmg_solver_destroy(mpmg_solver* s);
+
+int mpmg_solver_levels(const mpmg_solver* s);
+int mpmg_solver_level_info(const mpmg_solver* s, int level, mpmg_stencil* out);
+size_t mpmg_solver_unknowns(const mpmg_solver* s);
+void* mpmg_solver_stream(mpmg_solver* s);
+
+/* Manufactured right-hand side of the problem (assemble_rhs, mesh_fem.cpp:
+ * 157-202), computed on the host in binary64, compact ordering. */
+int mpmg_problem_rhs(int32_t dim, int32_t nodes, int32_t k, double* b_out);
+
+/* ir_solve with host buffers (b compact FP64 in, u compact FP64 out). The
+ * residual history (iterations+1 entries) is written when hist != NULL. */
+int mpmg_solver_solve(mpmg_solver* s, const double* b_host, double* u_host, const mpmg_solve_params* p,
+                      double* hist, int32_t hist_cap, mpmg_solve_report* rep);
+
+/* The solver's own device-resident padded FP64 rhs and solution buffers. */
+int mpmg_solver_device_buffers(mpmg_solver* s, double** b_dev, double** u_dev);
+
+/* Same, on device-resident padded FP64 vectors (b_dev, u_dev); passing the
+ * solver's own buffers (mpmg_solver_device_buffers) avoids any copy. */
+int mpmg_solver_solve_device(mpmg_solver* s, const double* b_dev, double* u_dev, const mpmg_solve_params* p,
+                             double* hist, int32_t hist_cap, mpmg_solve_report* rep);
+
+/* One V-cycle on host buffers: b, c compact in the finest level precision,
+ * passed as binary64 value-domain arrays (MgHierarchy::v_cycle). */
+int mpmg_solver_v_cycle(mpmg_solver* s, const double* b_host, double* c_host);
+
+/* Per-level operations on host value-domain buffers (for parity tests of the
+ * level kernels through the same device code the solver runs). */
+int mpmg_solver_level_op(mpmg_solver* s, int op, int level, const double* in0, const double* in1, double* out,
+                         int32_t steps, double scale);
+enum { MPMG_OP_SPMV = 0, MPMG_OP_JACOBI = 1, MPMG_OP_DEFECT = 2, MPMG_OP_RESTRICT = 3, MPMG_OP_PROLONG = 4,
+       MPMG_OP_COARSE_SOLVE = 5 };
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPMG_GPU_H */

@@ -1,0 +1,126 @@
+// Layer-1 C ABI (include/mpmg_gpu.h): one entry point per kernel family, on
+// device pointers in the padded layout. Argument checks mirror the
+// reference's `require` preconditions (kernels.cpp:243-395,
+// multigrid.cpp:79-280) and map to MPMG_EINVAL instead of exceptions.
+#include "mpmg_host.h"
+#include "mpmg_internal.h"
+
+using namespace mpmg_impl;
+
+namespace {
+
+bool valid_prec(int p) { return p == MPMG_FP16 || p == MPMG_FP32 || p == MPMG_FP64; }
+
+bool valid_stencil(const mpmg_stencil* A) {
+  return A && (A->dim == 2 || A->dim == 3) && A->nodes >= 3 && valid_prec(A->prec) &&
+         A->ntaps == (A->dim == 3 ? 27 : 9);
+}
+
+int rc(cudaError_t e) { return e == cudaSuccess ? MPMG_OK : set_cuda_error(e); }
+
+}  // namespace
+
+extern "C" {
+
+int mpmg_gpu_pack(int32_t dim, int32_t nodes, int32_t prec, const void* compact, void* padded, void* stream) {
+  if ((dim != 2 && dim != 3) || nodes < 3 || !valid_prec(prec) || !compact || !padded) return MPMG_EINVAL;
+  return rc(launch_pack(dim, nodes, prec, compact, padded, false, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_unpack(int32_t dim, int32_t nodes, int32_t prec, const void* padded, void* compact, void* stream) {
+  if ((dim != 2 && dim != 3) || nodes < 3 || !valid_prec(prec) || !compact || !padded) return MPMG_EINVAL;
+  return rc(launch_pack(dim, nodes, prec, compact, const_cast<void*>(padded), true, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_jacobi(const mpmg_stencil* A, const void* b, const void* u_in, void* u_out, double omega,
+                    uint32_t policy, void* stream) {
+  if (!valid_stencil(A) || !b || !u_out || u_in == u_out) return MPMG_EINVAL;
+  if (!(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;  // multigrid.cpp:82
+  if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (!u_in)
+    return rc(launch_jacobi_zero(A->dim, A->nodes, A->prec, b, u_out, round_to(omega, A->prec, policy & MPMG_FTZ),
+                                 A->inv_diag, policy, s));
+  return rc(launch_level_op(2, *A, u_in, b, u_out, omega, policy, s));
+}
+
+int mpmg_gpu_defect(const mpmg_stencil* A, const void* b, const void* u, void* r, uint32_t policy, void* stream) {
+  if (!valid_stencil(A) || !b || !u || !r || u == r) return MPMG_EINVAL;
+  if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
+  return rc(launch_level_op(1, *A, u, b, r, 1.0, policy, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_spmv(const mpmg_stencil* A, const void* x, void* y, uint32_t policy, void* stream) {
+  if (!valid_stencil(A) || !x || !y || x == y) return MPMG_EINVAL;  // kernels.cpp:248 aliasing
+  if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
+  return rc(launch_level_op(0, *A, x, nullptr, y, 1.0, policy, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_restrict(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_t coarse_prec, const void* r_fine,
+                      void* r_coarse, const double* scale_dev, uint32_t policy, void* stream) {
+  if ((dim != 2 && dim != 3) || fine_nodes < 5 || (fine_nodes - 1) % 2 || !valid_prec(fine_prec) ||
+      !valid_prec(coarse_prec) || !r_fine || !r_coarse)
+    return MPMG_EINVAL;
+  return rc(launch_restrict(dim, fine_nodes, fine_prec, coarse_prec, r_fine, r_coarse, scale_dev, policy,
+                            (cudaStream_t)stream));
+}
+
+int mpmg_gpu_prolong_correct(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_t coarse_prec,
+                             const void* c_coarse, void* u_fine, const double* scale_dev, uint32_t policy,
+                             void* stream) {
+  if ((dim != 2 && dim != 3) || fine_nodes < 5 || (fine_nodes - 1) % 2 || !valid_prec(fine_prec) ||
+      !valid_prec(coarse_prec) || !c_coarse || !u_fine)
+    return MPMG_EINVAL;
+  return rc(launch_prolong(dim, fine_nodes, fine_prec, coarse_prec, c_coarse, u_fine, scale_dev, policy,
+                           (cudaStream_t)stream));
+}
+
+int mpmg_gpu_defect_f64(const mpmg_stencil* A64, const double* b, const double* u, double* r, double* partials,
+                        void* stream) {
+  if (!valid_stencil(A64) || A64->prec != MPMG_FP64 || !b || !u || !r) return MPMG_EINVAL;
+  if (!stencil_supported(A64->dim, A64->nodes, MPMG_FP64)) return MPMG_EUNSUPPORTED;
+  return rc(launch_defect64(*A64, b, u, r, partials, true, false, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_update_rc(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, double* u,
+                       const double* alpha_dev, double* partials, uint32_t policy, void* stream) {
+  if (!valid_stencil(A64) || A64->prec != MPMG_FP64 || !c || !valid_prec(c_prec) || !r || !u || !alpha_dev)
+    return MPMG_EINVAL;
+  if (!stencil_supported(A64->dim, A64->nodes, c_prec)) return MPMG_EUNSUPPORTED;
+  return rc(launch_update_rc(*A64, c, c_prec, r, u, alpha_dev, partials, policy & MPMG_FMA, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_scale_downcast(int32_t dim, int32_t nodes, const double* x, void* out, int32_t prec,
+                            const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream) {
+  if ((dim != 2 && dim != 3) || nodes < 3 || !x || !out || !valid_prec(prec) || !alpha_dev) return MPMG_EINVAL;
+  return rc(launch_downcast(dim, nodes, x, out, prec, alpha_dev, scale_enabled, policy, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_partials_len(int32_t dim, int32_t nodes) {
+  const int a = stencil_partials(dim, nodes, MPMG_FP16), b = stencil_partials(dim, nodes, MPMG_FP32);
+  const int c = stencil_partials(dim, nodes, MPMG_FP64), d = norm2_partials(mpmg_padded_len(dim, nodes));
+  int m = a > b ? a : b;
+  m = m > c ? m : c;
+  return m > d ? m : d;
+}
+
+int mpmg_gpu_norm2_f64(int32_t dim, int32_t nodes, const double* x, double* partials, double* out_dev,
+                       void* stream) {
+  if ((dim != 2 && dim != 3) || nodes < 3 || !x || !partials || !out_dev) return MPMG_EINVAL;
+  return rc(launch_norm2(mpmg_padded_len(dim, nodes), x, partials, out_dev, (cudaStream_t)stream));
+}
+
+int mpmg_gpu_norm_finalize(const double* partials, int32_t n_partials, double* out_dev, void* stream) {
+  if (!partials || n_partials < 0 || !out_dev) return MPMG_EINVAL;
+  return rc(launch_norm_finalize(partials, n_partials, out_dev, (cudaStream_t)stream));
+}
+
+// level-0-style stencil for a grid/precision (MgHierarchy::build per level)
+int mpmg_build_stencil(int32_t dim, int32_t nodes, int32_t prec, uint32_t policy, mpmg_stencil* out) {
+  if (!out || !valid_prec(prec)) return MPMG_EINVAL;
+  return build_level_stencil(dim, nodes, prec, policy & MPMG_FTZ, out);
+}
+
+double mpmg_round_fp16(double x, int32_t ftz) { return round_fp16(x, ftz != 0); }
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// Internal host-side declarations shared by the CUDA translation units of the
+// B200 hot path. Not part of the public ABI (see include/mpmg_gpu.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "mpmg_gpu.h"
+
+namespace mpmg_impl {
+
+inline int pitch(int nodes) { return nodes - 1; }
+
+// binary16 RNE rounding with optional flush-after-rounding, in the binary64
+// value domain (same contract as the reference's quantize_fp16,
+// precision.cpp:23-48); host side, used to round per-level scalars.
+double round_fp16(double x, bool ftz);
+// PVector::set rounding (vector.hpp:43-55) to precision `prec`.
+double round_to(double x, int prec, bool ftz);
+uint16_t fp16_bits(double v);  // exact binary16 value -> bits
+double fp16_value(uint16_t bits);
+
+// ---- stencil family (mpmg_stencil_*.cu, mpmg_outer.cu) -------------------
+// level ops: op in {0 spmv, 1 defect, 2 jacobi}; level precision A.prec
+cudaError_t launch_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                            uint32_t policy, cudaStream_t s);
+cudaError_t launch_level_op_f16(int op, const mpmg_stencil& A, const void* x, const void* b, void* out,
+                                double omega, uint32_t policy, cudaStream_t s);
+cudaError_t launch_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out,
+                                double omega, uint32_t policy, cudaStream_t s);
+cudaError_t launch_level_op_f64(int op, const mpmg_stencil& A, const void* x, const void* b, void* out,
+                                double omega, uint32_t policy, cudaStream_t s);
+// outer FP64 ops
+cudaError_t launch_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
+                            bool fma, bool resnorm, cudaStream_t s, const int* gate = nullptr);
+cudaError_t launch_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
+                             const double* alpha_dev, double* partials, bool fma, cudaStream_t s);
+// number of partial sums the stencil kernels write for a grid (any LP)
+int stencil_partials(int dim, int nodes, int lp);
+// true when the streaming stencil kernels support this level shape
+bool stencil_supported(int dim, int nodes, int prec);
+
+// ---- pointwise / transfer (mpmg_pointwise.cu) -----------------------------
+cudaError_t launch_pack(int dim, int nodes, int prec, const void* compact, void* padded, bool unpack,
+                        cudaStream_t s);
+cudaError_t launch_jacobi_zero(int dim, int nodes, int prec, const void* b, void* u, double omega_r,
+                               double invdiag_r, uint32_t policy, cudaStream_t s);
+cudaError_t launch_restrict(int dim, int fine_nodes, int fine_prec, int coarse_prec, const void* r_fine,
+                            void* r_coarse, const double* scale_dev, uint32_t policy, cudaStream_t s);
+cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_prec, const void* c_coarse,
+                           void* u_fine, const double* scale_dev, uint32_t policy, cudaStream_t s);
+cudaError_t launch_downcast(int dim, int nodes, const double* x, void* out, int prec, const double* alpha_dev,
+                            int scale_enabled, uint32_t policy, cudaStream_t s);
+cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* out, cudaStream_t s);
+cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
+int norm2_partials(size_t len);
+cudaError_t launch_fill_random01(double* padded_u, int dim, int nodes, uint64_t seed, cudaStream_t s);
+
+// ---- coarse sub-hierarchy (mpmg_coarse.cu) --------------------------------
+constexpr int kMaxCoarseLevels = 16;
+struct CoarseLevel {
+  int dim, nodes, prec;
+  double taps[27];
+  double inv_diag;  // rounded to prec
+  double omega;     // rounded to prec
+  void *u, *u2, *b, *r;  // padded vectors of this level
+  double* prod;          // binary64 scratch (restriction products), interior-sized padded
+};
+struct CoarseArgs {
+  int nlev;          // levels 0..nlev-1 handled by the kernel
+  int pre, post;
+  int rescale;       // DSH restriction rescaling (multigrid.cpp:383)
+  double base_tol;
+  int base_mode, base_maxit;
+  CoarseLevel lv[kMaxCoarseLevels];
+  // CG scratch on level 0 (padded, level-0 precision) + best iterate
+  void *cg_r, *cg_p, *cg_ap, *cg_s, *cg_best;
+  int* cg_iterations;  // optional diagnostics (device)
+};
+cudaError_t launch_coarse_cycle(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
+
+// ---- IR control (mpmg_solver.cu) ------------------------------------------
+struct IrState {
+  double alpha;       // current ||r||
+  double scale;       // scale used by the current iteration
+  int iterations;
+  int converged;
+  int diverged;
+  int active;         // loop still running
+  int refresh_now;    // next refresh due
+  int pad;
+};
+
+std::string& last_error();
+int set_cuda_error(cudaError_t e);
+
+}  // namespace mpmg_impl

@@ -1,0 +1,343 @@
+// Pointwise and grid-transfer kernels of the hot path:
+//   * layout conversion compact <-> padded (mesh_fem.hpp:43-50 ordering),
+//   * first Jacobi step from u = 0 (multigrid.cpp:376 + 79-89),
+//   * full-weighting restriction with precision change (multigrid.cpp:236-268),
+//   * prolongation + correction (multigrid.cpp:270-280, 389-390),
+//   * scaled FP64 -> FP16/FP32 downcast (kernels.cpp:343-360),
+//   * deterministic two-stage FP64 norm (replaces kernels.cpp:384-395).
+#include <algorithm>
+
+#include "mpmg_arith.cuh"
+#include "mpmg_internal.h"
+
+namespace mpmg_impl {
+
+using namespace mpmg_dev;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned blocks_for(size_t n, int per_thread = 1) {
+  const size_t t = (n + (size_t)per_thread - 1) / per_thread;
+  return (unsigned)std::max<size_t>(1, (t + kThreads - 1) / kThreads);
+}
+
+template <int PREC> struct St;
+template <> struct St<P16> { using T = __half; };
+template <> struct St<P32> { using T = float; };
+template <> struct St<P64> { using T = double; };
+
+// padded index of interior point i of the compact ordering
+__device__ __forceinline__ long long padded_index(long long i, int dim, int P) {
+  const long long m = P - 1;
+  const long long x = i % m + 1;
+  if (dim == 2) return (i / m + 1) * P + x;
+  const long long y = (i / m) % m + 1, z = i / (m * m) + 1;
+  return (z * P + y) * (long long)P + x;
+}
+
+template <typename T>
+__global__ void k_pack(const T* __restrict__ src, T* __restrict__ dst, long long n, int dim, int P, int unpack) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long p = padded_index(i, dim, P);
+  if (unpack) dst[i] = src[p];
+  else dst[p] = src[i];
+}
+
+// u = round(omega * round(D^-1 * b)) == one Jacobi step from zero, bitwise:
+// t = A*0 = +0; r = fma(-1, +0, b) = b; t = d*b; u = fma(w, t, +0).
+template <int PREC, bool FTZ, bool FMA>
+__global__ void k_jacobi_zero(const void* __restrict__ bv, void* __restrict__ uv, long long len, double w,
+                              double d) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  if constexpr (PREC == P16) {
+    const __half b = static_cast<const __half*>(bv)[i];
+    const __half t = mul16s<FTZ>(__double2half(d), b);
+    static_cast<__half*>(uv)[i] = fma16s<FTZ, FMA>(__double2half(w), t, __ushort_as_half((unsigned short)0));
+  } else if constexpr (PREC == P32) {
+    const float b = static_cast<const float*>(bv)[i];
+    const float t = mul32<FTZ>((float)d, b);
+    static_cast<float*>(uv)[i] = fma32<FTZ, FMA>((float)w, t, 0.0f);
+  } else {
+    const double b = static_cast<const double*>(bv)[i];
+    static_cast<double*>(uv)[i] = fma64<FMA>(w, mul64(d, b), 0.0);
+  }
+}
+
+// transfer_product<P> single step (multigrid.cpp:166-195); weights exact
+template <int CP, bool FTZ, bool FMA> struct Xfer;
+template <bool FTZ, bool FMA> struct Xfer<P16, FTZ, FMA> {
+  using T = __half;
+  static __device__ __forceinline__ T zero() { return __ushort_as_half((unsigned short)0); }
+  static __device__ __forceinline__ T step(double w, T x, T acc) { return fma16s<FTZ, FMA>(__double2half(w), x, acc); }
+  static __device__ __forceinline__ double wide(T v) { return (double)__half2float(v); }
+};
+template <bool FTZ, bool FMA> struct Xfer<P32, FTZ, FMA> {
+  using T = float;
+  static __device__ __forceinline__ T zero() { return 0.0f; }
+  // multigrid.cpp:178-184: the unfused form rounds the product to binary32
+  // and flushes only the sum
+  static __device__ __forceinline__ T step(double w, T x, T acc) {
+    return f32<FTZ>(FMA ? __fmaf_rn((float)w, x, acc) : __fadd_rn(__fmul_rn((float)w, x), acc));
+  }
+  static __device__ __forceinline__ double wide(T v) { return (double)v; }
+};
+template <bool FTZ, bool FMA> struct Xfer<P64, FTZ, FMA> {
+  using T = double;
+  static __device__ __forceinline__ T zero() { return 0.0; }
+  static __device__ __forceinline__ T step(double w, T x, T acc) { return fma64<FMA>(w, x, acc); }
+  static __device__ __forceinline__ double wide(T v) { return v; }
+};
+
+template <int P, bool FTZ> __device__ __forceinline__ typename St<P>::T store_round(double v);
+template <> __device__ __forceinline__ __half store_round<P16, true>(double v) { return round16<true>(v); }
+template <> __device__ __forceinline__ __half store_round<P16, false>(double v) { return round16<false>(v); }
+template <> __device__ __forceinline__ float store_round<P32, true>(double v) { return round32<true>(v); }
+template <> __device__ __forceinline__ float store_round<P32, false>(double v) { return round32<false>(v); }
+template <> __device__ __forceinline__ double store_round<P64, true>(double v) { return v; }
+template <> __device__ __forceinline__ double store_round<P64, false>(double v) { return v; }
+
+// restriction: one thread per coarse interior node (cx,cy,cz); 3^dim fine
+// neighbours of (2cx,2cy,2cz) in lexicographic order with weights
+// prod_d (d == 0 ? 1 : 1/2) (mesh_fem.cpp:266-293).
+template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
+__global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_, int Pc, const double* scale_dev) {
+  using X = Xfer<FP, FTZ, FMA>;
+  using TF = typename X::T;
+  const TF* rf = static_cast<const TF*>(rf_);
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int cy = blockIdx.y * blockDim.y + threadIdx.y + 1;
+  const int cz = DIM == 3 ? (int)blockIdx.z + 1 : 0;
+  if (cx > Pc - 1 || cy > Pc - 1) return;
+  const int Pf = 2 * Pc;
+  const long long pf = DIM == 3 ? (long long)Pf * Pf : (long long)Pf;
+  TF acc = X::zero();
+  const long long cf = (DIM == 3 ? (long long)(2 * cz) * pf : 0) + (long long)(2 * cy) * Pf + 2 * cx;
+#pragma unroll
+  for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const double w = (dx == 0 ? 1.0 : 0.5) * (dy == 0 ? 1.0 : 0.5) * (dz == 0 ? 1.0 : 0.5);
+        acc = X::step(w, rf[cf + dz * pf + (long long)dy * Pf + dx], acc);
+      }
+  const double s = scale_dev ? *scale_dev : 1.0;
+  const double v = X::wide(acc) / s;
+  const long long ci = (DIM == 3 ? (long long)cz * Pc * Pc : 0) + (long long)cy * Pc + cx;
+  static_cast<typename St<CPc>::T*>(rc_)[ci] = store_round<CPc, FTZ>(v);
+}
+
+// prolongation + correction: one thread per fine interior node; parents per
+// dimension: even j -> j/2 (w 1), odd -> (j-1)/2, (j+1)/2 (w 1/2), z-parent
+// outermost (mesh_fem.cpp:222-252). Boundary parents read the stored zeros.
+template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
+__global__ void k_prolong(const void* __restrict__ cc_, void* __restrict__ uf_, int Pf, const double* scale_dev) {
+  using X = Xfer<CPc, FTZ, FMA>;
+  using TC = typename X::T;
+  const TC* cc = static_cast<const TC*>(cc_);
+  const int fx = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int fy = blockIdx.y * blockDim.y + threadIdx.y + 1;
+  const int fz = DIM == 3 ? (int)blockIdx.z + 1 : 0;
+  if (fx > Pf - 1 || fy > Pf - 1) return;
+  const int Pc = Pf / 2;
+  int px[2], py[2], pz[2];
+  double wx, wy, wz;
+  const int nx = (fx & 1) ? 2 : 1, ny = (fy & 1) ? 2 : 1, nz = DIM == 3 ? ((fz & 1) ? 2 : 1) : 1;
+  px[0] = fx >> 1; px[1] = (fx + 1) >> 1; wx = (fx & 1) ? 0.5 : 1.0;
+  py[0] = fy >> 1; py[1] = (fy + 1) >> 1; wy = (fy & 1) ? 0.5 : 1.0;
+  pz[0] = fz >> 1; pz[1] = (fz + 1) >> 1; wz = DIM == 3 ? ((fz & 1) ? 0.5 : 1.0) : 1.0;
+  TC acc = X::zero();
+  for (int c = 0; c < nz; ++c)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a) {
+        const long long ci = (DIM == 3 ? (long long)pz[c] * Pc * Pc : 0) + (long long)py[b] * Pc + px[a];
+        acc = X::step(wx * wy * wz, cc[ci], acc);
+      }
+  const double s = scale_dev ? *scale_dev : 1.0;
+  const double v = X::wide(acc) * s;
+  const long long fi = (DIM == 3 ? (long long)fz * Pf * Pf : 0) + (long long)fy * Pf + fx;
+  using TF = typename St<FP>::T;
+  TF* uf = static_cast<TF*>(uf_);
+  const TF t = store_round<FP, FTZ>(v);
+  if constexpr (FP == P16) uf[fi] = fma16s<FTZ, FMA>(__ushort_as_half((unsigned short)0x3C00), t, uf[fi]);
+  else if constexpr (FP == P32) uf[fi] = fma32<FTZ, FMA>(1.0f, t, uf[fi]);
+  else uf[fi] = fma64<FMA>(1.0, t, uf[fi]);
+}
+
+// out = round_prec(x / s), s = (scale_enabled && alpha > 0) ? alpha : 1
+template <int PREC, bool FTZ>
+__global__ void k_downcast(const double* __restrict__ x, void* __restrict__ out, long long len,
+                           const double* alpha, int scale_enabled) {
+  const double a = *alpha;
+  const double s = (scale_enabled && a > 0.0) ? a : 1.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+    static_cast<typename St<PREC>::T*>(out)[i] = store_round<PREC, FTZ>(__ddiv_rn(x[i], s));
+}
+
+// deterministic per-block partial sums of x_i^2 (fixed grid, fixed order)
+__global__ void k_sumsq(const double* __restrict__ x, long long len, double* partials) {
+  __shared__ double red[kThreads / 32];
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+    acc = __fma_rn(x[i], x[i], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_finalize(const double* __restrict__ partials, int n, double* out) {
+  __shared__ double red[kThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads) acc += partials[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sqrt(red[0]);
+}
+
+// SplitMix64 U[0,1) initial guess (ir_solver.cpp:80-84, rng.hpp:13-25): the
+// k-th interior node (compact order) receives the k-th draw.
+__global__ void k_random01(double* u, long long n, int dim, int P, uint64_t seed) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  u[padded_index(i, dim, P)] = (double)(z >> 11) * 0x1.0p-53;
+}
+
+template <typename F>
+cudaError_t with_ftz_fma(uint32_t policy, F&& f) {
+  const bool ftz = policy & MPMG_FTZ, fma = policy & MPMG_FMA;
+  if (ftz && fma) return f(std::true_type{}, std::true_type{});
+  if (ftz) return f(std::true_type{}, std::false_type{});
+  if (fma) return f(std::false_type{}, std::true_type{});
+  return f(std::false_type{}, std::false_type{});
+}
+
+template <typename F>
+cudaError_t with_prec(int prec, F&& f) {
+  switch (prec) {
+    case MPMG_FP16: return f(std::integral_constant<int, P16>{});
+    case MPMG_FP32: return f(std::integral_constant<int, P32>{});
+    default: return f(std::integral_constant<int, P64>{});
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_pack(int dim, int nodes, int prec, const void* compact, void* padded, bool unpack,
+                        cudaStream_t s) {
+  const size_t n = mpmg_interior_len(dim, nodes);
+  if (n == 0) return cudaSuccess;
+  const int P = pitch(nodes);
+  return with_prec(prec, [&](auto pc) -> cudaError_t {
+    using T = typename St<decltype(pc)::value>::T;
+    if (unpack)
+      k_pack<T><<<blocks_for(n), kThreads, 0, s>>>(static_cast<const T*>(padded), static_cast<T*>(const_cast<void*>(compact)),
+                                                    (long long)n, dim, P, 1);
+    else
+      k_pack<T><<<blocks_for(n), kThreads, 0, s>>>(static_cast<const T*>(compact), static_cast<T*>(padded), (long long)n,
+                                                    dim, P, 0);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_jacobi_zero(int dim, int nodes, int prec, const void* b, void* u, double omega_r,
+                               double invdiag_r, uint32_t policy, cudaStream_t s) {
+  const size_t len = mpmg_padded_len(dim, nodes);
+  return with_prec(prec, [&](auto pc) -> cudaError_t {
+    return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+      k_jacobi_zero<decltype(pc)::value, decltype(ft)::value, decltype(fm)::value>
+          <<<blocks_for(len), kThreads, 0, s>>>(b, u, (long long)len, omega_r, invdiag_r);
+      return cudaGetLastError();
+    });
+  });
+}
+
+cudaError_t launch_restrict(int dim, int fine_nodes, int fine_prec, int coarse_prec, const void* r_fine,
+                            void* r_coarse, const double* scale_dev, uint32_t policy, cudaStream_t s) {
+  const int Pc = pitch(fine_nodes) / 2;
+  if (Pc < 2) return cudaSuccess;
+  const dim3 block(32, 8);
+  const dim3 grid((Pc - 1 + 31) / 32, (Pc - 1 + 7) / 8, dim == 3 ? Pc - 1 : 1);
+  return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
+    return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
+      return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+        constexpr int F = decltype(fp)::value, Cc = decltype(cp)::value;
+        constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
+        if (dim == 3) k_restrict<3, F, Cc, T, M><<<grid, block, 0, s>>>(r_fine, r_coarse, Pc, scale_dev);
+        else k_restrict<2, F, Cc, T, M><<<grid, block, 0, s>>>(r_fine, r_coarse, Pc, scale_dev);
+        return cudaGetLastError();
+      });
+    });
+  });
+}
+
+cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_prec, const void* c_coarse,
+                           void* u_fine, const double* scale_dev, uint32_t policy, cudaStream_t s) {
+  const int Pf = pitch(fine_nodes);
+  const dim3 block(32, 8);
+  const dim3 grid((Pf - 1 + 31) / 32, (Pf - 1 + 7) / 8, dim == 3 ? Pf - 1 : 1);
+  return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
+    return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
+      return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+        constexpr int F = decltype(fp)::value, Cc = decltype(cp)::value;
+        constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
+        if (dim == 3) k_prolong<3, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
+        else k_prolong<2, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
+        return cudaGetLastError();
+      });
+    });
+  });
+}
+
+cudaError_t launch_downcast(int dim, int nodes, const double* x, void* out, int prec, const double* alpha_dev,
+                            int scale_enabled, uint32_t policy, cudaStream_t s) {
+  const size_t len = mpmg_padded_len(dim, nodes);
+  const unsigned blocks = std::min<unsigned>(blocks_for(len, 4), 148u * 16u);
+  return with_prec(prec, [&](auto pc) -> cudaError_t {
+    if (policy & MPMG_FTZ)
+      k_downcast<decltype(pc)::value, true><<<blocks, kThreads, 0, s>>>(x, out, (long long)len, alpha_dev, scale_enabled);
+    else
+      k_downcast<decltype(pc)::value, false><<<blocks, kThreads, 0, s>>>(x, out, (long long)len, alpha_dev, scale_enabled);
+    return cudaGetLastError();
+  });
+}
+
+int norm2_partials(size_t len) { return (int)std::min<unsigned>(blocks_for(len, 8), 148u * 8u); }
+
+cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* out, cudaStream_t s) {
+  const int nb = norm2_partials(len);
+  k_sumsq<<<nb, kThreads, 0, s>>>(x, (long long)len, partials);
+  k_finalize<<<1, kThreads, 0, s>>>(partials, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s) {
+  k_finalize<<<1, kThreads, 0, s>>>(partials, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_random01(double* padded_u, int dim, int nodes, uint64_t seed, cudaStream_t s) {
+  const size_t n = mpmg_interior_len(dim, nodes);
+  if (n == 0) return cudaSuccess;
+  k_random01<<<blocks_for(n), kThreads, 0, s>>>(padded_u, (long long)n, dim, pitch(nodes), seed);
+  return cudaGetLastError();
+}
+
+}  // namespace mpmg_impl
