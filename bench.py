@@ -1,0 +1,470 @@
+"""Benchmark of the B200 hot path (BASELINE.json metric):
+
+  "IR-MG time to 1e-10 rel. residual (s), FP16/mixed vs FP64; kernel HBM GB/s"
+
+Workload (BASELINE.json configs[1]): 3D Poisson on the unit cube, 257^3 nodes
+(255^3 = 16,581,375 unknowns), L = 8 levels, V(3,3) damped Jacobi (omega 2/3),
+FP64 iterative refinement preconditioned by one pure-binary16 V-cycle with
+residuum scaling (H_MG), u0 = 0, stopping at ||r||_2 <= 1e-10 ||b||_2. The
+same solver in all-binary64 (D_MG, the same fused kernels at 8 bytes/value) is
+timed beside it. Arithmetic policy: flush_subnormals_to_zero = false,
+fused_multiply_add = true (SURVEY §7 hard part 2; the reference default
+flushes, `--ftz 1` selects it).
+
+One "step" = one complete ir_solve (device-resident inputs for `value`; host
+buffers through the C ABI for `e2e`). Every FP64 level vector of the finest
+grid is 133 MB and the three of them exceed the 126 MB L2; the L2 is
+additionally flushed (a 512 MiB write) before every timed solve.
+
+`--impl reference` times the reference's own CPU implementation (the
+unmodified library compiled from /root/reference into oracle/_ref/) on a
+bounded sample of the same workload: see cpu_reference() below.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IR-MG time to 1e-10 rel. residual (s), FP16/mixed vs FP64; kernel HBM GB/s"
+UNIT = "s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dim", type=int, default=3)
+    ap.add_argument("--nodes", type=int, default=257)
+    ap.add_argument("--levels", type=int, default=0, help="0 = max depth (base 3 nodes/dim)")
+    ap.add_argument("--variant", default="h_mg", choices=["h_mg", "hsd_mg", "dsh_mg", "d_mg"])
+    ap.add_argument("--ftz", type=int, default=0)
+    ap.add_argument("--pre", type=int, default=3)
+    ap.add_argument("--post", type=int, default=3)
+    ap.add_argument("--rel-tol", type=float, default=1e-10)
+    ap.add_argument("--no-fp64", action="store_true", help="skip the all-FP64 comparison solve")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline timing")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--only-kernels", action="store_true", help="per-kernel timing only (for ncu captures)")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="host-driven IR loop instead of the graph WHILE node (ncu cannot profile conditional graphs)")
+    return ap.parse_args()
+
+
+def max_depth(n):
+    L = 1
+    while ((n - 1) >> L) >= 2 and ((n - 1) % (1 << L)) == 0:
+        L += 1
+    return L
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks: nvidia-smi sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+        self.path = os.path.join("/tmp", f"mpmg_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 10:
+                    continue
+                try:
+                    rows.append(parts)
+                except Exception:
+                    pass
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        load = [r for r in rows if (num(r[3]) or 0) >= 50] or rows
+        sm = sorted(num(r[1]) for r in load if num(r[1]) is not None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[6 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": num(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": max((num(r[4]) or 0) for r in rows)}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(a):
+    import numpy as np
+    import torch
+
+    import paper_2007_07539_b200 as mg
+
+    ws, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    L = a.levels or max_depth(a.nodes)
+    dim, n = a.dim, a.nodes
+    N = mg.unknowns(dim, n)
+    ftz = bool(a.ftz)
+    lib = mg.lib()
+
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def flush_l2():
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+
+    # host problem setup (assemble_rhs on the host, once)
+    b = mg.problem_rhs(dim, n)
+    tol = a.rel_tol * float(np.sqrt(np.dot(b, b)))
+    cfgs = [(a.variant, "mixed")] + ([] if (a.no_fp64 or a.variant == "d_mg") else [("d_mg", "fp64")])
+    if a.only_kernels:
+        print(json.dumps(kernel_roofline(a, dim, n, L, ftz, dev, flush_l2)))
+        return
+    results = {}
+    sampler = ClockSampler(local)
+    launches_per_solve = {}
+    for variant, tag in cfgs:
+        h = mg.Hierarchy(dim, n, L, variant, pre=a.pre, post=a.post, ftz=ftz, device=local)
+        bd, ud = h.device_buffers()
+        # upload the rhs into the solver's padded FP64 buffer
+        bt = torch.from_numpy(b).to(dev)
+        torch.cuda.synchronize()
+        mg._check(lib.mpmg_gpu_pack(dim, n, mg.FP64, bt.data_ptr(), bd, None), "pack")
+        torch.cuda.synchronize()
+        cfg = mg.IrConfig(outer_tolerance=tol, use_graph=not a.no_graph)
+        for _ in range(a.warmup):
+            flush_l2()
+            rep = h.ir_solve_ptr(bd, ud, cfg, device=True)
+        if tag == "mixed":
+            sampler.start()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        times, its = [], []
+        for _ in range(a.steps):
+            flush_l2()
+            rep = h.ir_solve_ptr(bd, ud, cfg, device=True)  # CUDA events on the solver stream
+            times.append(rep.device_seconds)
+            its.append(rep.iterations)
+            assert rep.converged, f"{variant} did not converge"
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        t = float(np.mean(times))
+        if ws > 1:
+            tt = torch.tensor([t], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt.item())
+        results[tag] = dict(variant=variant, seconds=t, iterations=int(its[-1]), min_s=float(np.min(times)),
+                            final_residual=rep.final_residual)
+        launches_per_solve[tag] = solve_launches(h, its[-1], a)
+        if tag == "mixed":
+            # e2e through the public C ABI with pinned HOST buffers: H2D of b,
+            # pack, solve, unpack, D2H of u inside the timed region
+            bh = torch.from_numpy(b).pin_memory()
+            uh = torch.empty(N, dtype=torch.float64).pin_memory()
+            for _ in range(max(1, a.warmup)):
+                flush_l2()
+                h.ir_solve_ptr(bh.data_ptr(), uh.data_ptr(), cfg, device=False)
+            e2e = []
+            for _ in range(a.steps):
+                flush_l2()
+                t0 = time.perf_counter()
+                rep = h.ir_solve_ptr(bh.data_ptr(), uh.data_ptr(), cfg, device=False)
+                e2e.append(time.perf_counter() - t0)
+            e2e_t = float(np.mean(e2e))
+            if ws > 1:
+                tt = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+                torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+                e2e_t = float(tt.item())
+            results["e2e"] = e2e_t
+        h.close()
+        del bt
+        torch.cuda.empty_cache()
+
+    kernels = {} if a.no_kernels else kernel_roofline(a, dim, n, L, ftz, dev, flush_l2)
+    clocks = sampler.stop()
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+    mix = results["mixed"]
+    peaks = load_peaks()
+    out = {
+        "metric": METRIC, "value": mix["seconds"], "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": mix["seconds"] * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp16" if a.variant == "h_mg" else "mixed fp16/fp32/fp64",
+        "data": "synthetic: the reference's own manufactured Poisson problem (assemble_rhs k=1), u0 = 0",
+        "config": {"workload": f"{dim}D Poisson {n}^{dim} ({N} unknowns), L={L}, V({a.pre},{a.post}) Jacobi "
+                               f"w=2/3, {a.variant.upper()} preconditioned FP64 IR to {a.rel_tol:g}*||b||",
+                   "variant": a.variant, "policy": {"flush_subnormals_to_zero": ftz, "fused_multiply_add": True,
+                                                    "fp16_accumulation": "fp16"},
+                   "l2": "flushed (512 MiB write) before every timed solve; finest FP64 vectors 3x133 MB > L2",
+                   "parallelism": "replicas only (one independent solve per GPU)" if ws > 1 else "1 GPU"},
+        "iterations": mix["iterations"],
+        "final_residual": mix["final_residual"],
+        "tolerance": tol,
+    }
+    if "fp64" in results:
+        d = results["fp64"]
+        out["fp64_baseline"] = {"variant": "d_mg", "seconds": d["seconds"], "iterations": d["iterations"],
+                                "speedup_mixed_vs_fp64": d["seconds"] / mix["seconds"]}
+    out["e2e"] = {"value": results["e2e"], "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                  "d2h_bytes_per_step": 8 * N + 32 + 8,  # solution + IR state + final norm
+                  "path": "mpmg_solver_solve (C ABI, pinned host b/u)"}
+    out["gpu_launches"] = launches_per_solve["mixed"] * a.steps
+    out["gpu_launches_per_solve"] = launches_per_solve
+    if kernels:
+        dom = kernels[kernels["dominant"]]
+        out["roofline"] = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peaks["hbm_gbs"],
+                           "unit": "GB/s", "frac": dom["achieved_gbs"] / peaks["hbm_gbs"],
+                           "traffic": dom.get("traffic"), "kernel": kernels["dominant"],
+                           "algorithmic_bytes": dom["bytes"], "avg_us": dom["avg_us"],
+                           "peak_source": peaks["source"]}
+        out["kernels"] = {k: v for k, v in kernels.items() if k != "dominant"}
+    out["clocks"] = clocks
+    if not a.no_cpu and ws == 1:
+        try:
+            out["cpu_baseline"] = cpu_reference(a, dim, n, L, ftz, mix["iterations"], steps=1)
+        except Exception as ex:  # reported, not fatal
+            out["cpu_baseline"] = {"error": str(ex)[:200]}
+    print(json.dumps(out), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def solve_launches(h, iterations, a):
+    """Kernels launched by one graph-captured solve (see mpmg_solver.cu):
+    init = state reset + FP64 defect + control; per iteration = downcast +
+    per streaming level (pre + post Jacobi steps, defect, restriction,
+    prolongation) + one coarse-CTA kernel + update_rc + gated refresh defect +
+    control; final = residual-norm defect + finalize."""
+    lib = h  # noqa
+    big = 0
+    for l in range(h.levels):
+        if ((h.level_nodes(l) - 1) >= 64):
+            big += 1
+    per_level = a.pre + a.post + 3
+    per_it = 1 + big * per_level + 1 + 1 + 1 + 1
+    return 3 + iterations * per_it + 2
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def kernel_roofline(a, dim, n, L, ftz, dev, flush_l2):
+    """Per-launch CUDA-event timing of the finest-level kernels, L2 flushed
+    before every launch, on the stream they are launched on. Algorithmic
+    bytes per launch (each operand read/written once, N = interior
+    unknowns of the finest level):
+      jacobi (binary16, 27-pt)      3 * 2 * N   (read u, b; write u')
+      update_rc (FP64 r,u; fp16 c)  (32 + 2) N  (read c, r, u; write r, u)
+      downcast (FP64 -> binary16)   (8 + 2) N
+      defect64 (FP64)               24 N        (read u, b; write r)
+    """
+    import torch
+
+    import paper_2007_07539_b200 as mg
+    lib = mg.lib()
+    N = mg.unknowns(dim, n)
+    plen = lib.mpmg_padded_len(dim, n)
+    prec = {"h_mg": mg.FP16, "hsd_mg": mg.FP16, "dsh_mg": mg.FP64, "d_mg": mg.FP64}[a.variant]
+    pb = mg.Hierarchy.__init__  # noqa (documentation)
+    pol = mg.policy_word(ftz, True, False)
+    A = mg.level_stencil(dim, n, prec, ftz)
+    A64 = mg.level_stencil(dim, n, mg.FP64, ftz)
+    tdt = torch.float16 if prec == mg.FP16 else torch.float64
+    g = torch.Generator(device=dev).manual_seed(1)
+    scale = 1.0 / (N ** 0.5)
+
+    def padded(dt, p):
+        comp = ((torch.rand(N, device=dev, generator=g, dtype=torch.float64) * 2 - 1) * scale).to(dt)
+        out = torch.zeros(plen, dtype=dt, device=dev)
+        mg._check(lib.mpmg_gpu_pack(dim, n, p, comp.data_ptr(), out.data_ptr(), None), "pack")
+        return out
+
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    u = padded(tdt, prec); b = padded(tdt, prec); u2 = torch.zeros_like(u)
+    r64 = padded(torch.float64, mg.FP64); u64 = padded(torch.float64, mg.FP64)
+    b64 = padded(torch.float64, mg.FP64)
+    alpha = torch.tensor([1e-3], dtype=torch.float64, device=dev)
+    part = torch.zeros(lib.mpmg_gpu_partials_len(dim, n), dtype=torch.float64, device=dev)
+    bp = 2 if prec == mg.FP16 else 8
+    specs = {
+        "jacobi_fine": (3 * bp * N, lambda: lib.mpmg_gpu_jacobi(C.byref(A), b.data_ptr(), u.data_ptr(),
+                                                                u2.data_ptr(), 2.0 / 3.0, pol, sp)),
+        "update_rc": ((32 + bp) * N, lambda: lib.mpmg_gpu_update_rc(C.byref(A64), u.data_ptr(), prec,
+                                                                    r64.data_ptr(), u64.data_ptr(),
+                                                                    alpha.data_ptr(), part.data_ptr(), pol, sp)),
+        "downcast": ((8 + bp) * N, lambda: lib.mpmg_gpu_scale_downcast(dim, n, r64.data_ptr(), u2.data_ptr(), prec,
+                                                                       alpha.data_ptr(), 1, pol, sp)),
+        "defect64": (24 * N, lambda: lib.mpmg_gpu_defect_f64(C.byref(A64), b64.data_ptr(), u64.data_ptr(),
+                                                              r64.data_ptr(), part.data_ptr(), sp)),
+    }
+    res = {}
+    for name, (nbytes, fn) in specs.items():
+        for _ in range(3):
+            mg._check(fn(), name)
+        ts = []
+        for _ in range(a.kernel_reps):
+            flush_l2()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mg._check(fn(), name)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        avg = sum(ts) / len(ts)
+        res[name] = {"bytes": nbytes, "avg_us": avg * 1e6, "achieved_gbs": nbytes / avg / 1e9}
+    # the kernel with the largest share of a solve: update_rc runs once per
+    # iteration, the finest Jacobi (pre + post - 1) times (first step from 0
+    # is a separate kernel)
+    share = {"jacobi_fine": res["jacobi_fine"]["avg_us"] * (a.pre + a.post - 1),
+             "update_rc": res["update_rc"]["avg_us"], "downcast": res["downcast"]["avg_us"],
+             "defect64": res["defect64"]["avg_us"] / 10.0}
+    res["dominant"] = max(share, key=share.get)
+    for k in share:
+        res[k]["us_per_iteration"] = share[k]
+    return res
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the unmodified reference library)
+# ---------------------------------------------------------------------------
+CPU_SAMPLE_NODES = 129   # 127^3 = 2,048,383 unknowns, L = 7
+CPU_SAMPLE_ITS = 2
+# outer-iteration counts the reference itself needs at 257^3, u0 = 0, tol
+# 1e-10||b|| (measured by running the reference)
+REF_ITS_257 = {("h_mg", False): 10, ("d_mg", False): 7, ("d_mg", True): 7}
+
+
+def cpu_reference(a, dim, n, L, ftz, gpu_iterations, steps=1):
+    """Times the reference's ir_solve on the host (single-threaded library,
+    1 core) on a bounded sample: the same variant/policy/smoother at 129^3
+    (L=7), CPU_SAMPLE_ITS outer iterations (hierarchy build excluded, as in
+    the reference's own SolveReport.wall_time_s). Scaled to the workload:
+    seconds/iteration x (N_257 / N_129) x iterations the reference needs at
+    257^3 (falls back to the GPU's count when no reference count is pinned)."""
+    from oracle import Reference
+    R = Reference()
+    sn = CPU_SAMPLE_NODES if n > CPU_SAMPLE_NODES else n
+    sL = max_depth(sn)
+    hr = R.hierarchy(dim, sn, sL, a.variant, pre=a.pre, post=a.post, ftz=ftz)
+    walls = []
+    for _ in range(steps):
+        res = hr.ir_solve(rel_tol=a.rel_tol, max_it=CPU_SAMPLE_ITS, want_u=False)
+        walls.append(res["wall_s"])
+    per_it = min(walls) / max(1, res["iterations"])
+    Ns = (sn - 2) ** dim
+    Nf = (n - 2) ** dim
+    its = REF_ITS_257.get((a.variant, ftz), gpu_iterations) if n == 257 else gpu_iterations
+    value = per_it * (Nf / Ns) * its
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"reference ir_solve (oracle/_ref, unmodified library) at {sn}^{dim} L={sL}, "
+                      f"{res['iterations']} outer its, {per_it:.3f} s/it; x{Nf / Ns:.3f} unknowns x {its} its "
+                      f"(reference count at {n}^{dim})",
+            "sample_wall_s": sum(walls), "build_s": hr.build_seconds}
+
+
+def run_reference(a):
+    ws, rank, _ = dist_info()
+    if ws > 1 and rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    L = a.levels or max_depth(a.nodes)
+    ftz = bool(a.ftz)
+    try:
+        from oracle import Reference
+        Reference()
+    except Exception as ex:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {ex}"[:200]}))
+        return
+    vals = []
+    t0 = time.perf_counter()
+    for i in range(a.warmup + a.steps):
+        cb = cpu_reference(a, a.dim, a.nodes, L, ftz, REF_ITS_257.get((a.variant, ftz), 10), steps=1)
+        if i >= a.warmup:
+            vals.append(cb["value"])
+    v = sum(vals) / len(vals)
+    N = (a.nodes - 2) ** a.dim
+    cb["value"] = v
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "fp16 (software-emulated)" if a.variant == "h_mg" else "fp64",
+           "data": "synthetic: the reference's manufactured Poisson problem",
+           "config": {"workload": f"{a.dim}D Poisson {a.nodes}^{a.dim} ({N} unknowns), L={L}, V({a.pre},{a.post}),"
+                                  f" {a.variant.upper()} IR to {a.rel_tol:g}*||b||", "variant": a.variant,
+                      "policy": {"flush_subnormals_to_zero": ftz, "fused_multiply_add": True}},
+           "cpu_baseline": cb,
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": time.perf_counter() - t0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

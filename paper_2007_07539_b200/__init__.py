@@ -121,6 +121,24 @@ def lib():
     L.mpmg_solver_v_cycle.restype = i; L.mpmg_solver_v_cycle.argtypes = [vp, dp, dp]
     L.mpmg_solver_level_op.restype = i
     L.mpmg_solver_level_op.argtypes = [vp, i, i, dp, dp, dp, i32, d]
+    # layer 1: kernel entry points on raw device pointers (padded layout)
+    sp = C.POINTER(Stencil)
+    L.mpmg_gpu_pack.restype = i; L.mpmg_gpu_pack.argtypes = [i32, i32, i32, vp, vp, vp]
+    L.mpmg_gpu_unpack.restype = i; L.mpmg_gpu_unpack.argtypes = [i32, i32, i32, vp, vp, vp]
+    L.mpmg_gpu_jacobi.restype = i; L.mpmg_gpu_jacobi.argtypes = [sp, vp, vp, vp, d, u32, vp]
+    L.mpmg_gpu_defect.restype = i; L.mpmg_gpu_defect.argtypes = [sp, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_spmv.restype = i; L.mpmg_gpu_spmv.argtypes = [sp, vp, vp, u32, vp]
+    L.mpmg_gpu_restrict.restype = i
+    L.mpmg_gpu_restrict.argtypes = [i32, i32, i32, i32, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_prolong_correct.restype = i
+    L.mpmg_gpu_prolong_correct.argtypes = [i32, i32, i32, i32, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_defect_f64.restype = i; L.mpmg_gpu_defect_f64.argtypes = [sp, vp, vp, vp, vp, vp]
+    L.mpmg_gpu_update_rc.restype = i; L.mpmg_gpu_update_rc.argtypes = [sp, vp, i32, vp, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_scale_downcast.restype = i
+    L.mpmg_gpu_scale_downcast.argtypes = [i32, i32, vp, vp, i32, vp, i32, u32, vp]
+    L.mpmg_gpu_partials_len.restype = i; L.mpmg_gpu_partials_len.argtypes = [i32, i32]
+    L.mpmg_gpu_norm2_f64.restype = i; L.mpmg_gpu_norm2_f64.argtypes = [i32, i32, vp, vp, vp, vp]
+    L.mpmg_gpu_norm_finalize.restype = i; L.mpmg_gpu_norm_finalize.argtypes = [vp, i32, vp, vp]
     _lib = L
     return L
 
