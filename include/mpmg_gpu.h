@@ -15,7 +15,7 @@
  *     V-cycle, IR solve) with HOST buffers, mirroring MgHierarchy::build
  *     (multigrid.hpp:104-107), MgHierarchy::v_cycle (multigrid.hpp:119) and
  *     ir_solve (ir_solver.hpp:57-60). This is what an FFI (ctypes/cgo/JNI)
- *     binds; the C++ drop-in API (include/mpmg/*.hpp) is built on it.
+ *     binds; the C++ drop-in API (include/mpmg/ headers) is built on it.
  *
  * Device vector layout ("ghost-aliased pitch layout"). A level with n nodes
  * per dimension (boundary included) has pitch P = n - 1 and stores node
@@ -137,6 +137,55 @@ int mpmg_gpu_partials_len(int32_t dim, int32_t nodes);
 int mpmg_gpu_norm2_f64(int32_t dim, int32_t nodes, const double* x, double* partials, double* out_dev,
                        void* stream);
 int mpmg_gpu_norm_finalize(const double* partials, int32_t n_partials, double* out_dev, void* stream);
+
+/* ---- generic ELLPACK path (from_levels hierarchies, public kernel API) ----
+ * Device matrices are SLOT-MAJOR: val[s*rows + r], col[s*rows + r] (the
+ * reference's row-major EllMatrix, ell_matrix.hpp:18-74, transposed on
+ * upload so that a warp's 32 rows read one coalesced segment per slot).
+ * Vectors are dense device arrays in their storage precision. */
+
+/* y = A x in precision prec, per-slot rounding in slot order (spmv_impl,
+ * kernels.cpp:137-193); MPMG_ACC32 in `policy` selects Fp16Accum::FP32 for
+ * binary16 data. x and y must differ (kernels.cpp:248). */
+int mpmg_gpu_ell_spmv(int64_t rows, int32_t rw, const int32_t* col, const void* val, int32_t prec, const void* x,
+                      void* y, uint32_t policy, void* stream);
+/* out = y + round(alpha) x (axpy_impl, kernels.cpp:195-212); out may alias */
+int mpmg_gpu_axpy(int64_t n, int32_t prec, double alpha, const void* x, const void* y, void* out, uint32_t policy,
+                  void* stream);
+/* out = a .* b (vec_multiply_impl, kernels.cpp:214-229); out may alias */
+int mpmg_gpu_vec_multiply(int64_t n, int32_t prec, const void* a, const void* b, void* out, uint32_t policy,
+                          void* stream);
+/* transfer_product + store_scaled (multigrid.cpp:155-232): the product M x in
+ * x's precision (matrix values re-rounded to it), then out = round_out(prod /
+ * scale) when divide != 0 (restriction) or round_out(prod * scale)
+ * (prolongation). scale_dev NULL = 1. prod (optional, binary64) receives the
+ * products for the DSH rescale norm. */
+int mpmg_gpu_ell_transfer(int64_t rows, int32_t rw, const int32_t* col, const void* val, int32_t mat_prec,
+                          const void* x, int32_t x_prec, int32_t out_prec, const double* scale_dev, int32_t divide,
+                          void* out, double* prod, uint32_t policy, void* stream);
+/* update_residuum_correction on a generic binary64 ELL (kernels.cpp:300-341) */
+int mpmg_gpu_ell_update_rc(int64_t rows, int32_t rw, const int32_t* col, const double* val, const void* c,
+                           int32_t c_prec, double* r, double* u, const double* alpha_dev, uint32_t policy,
+                           void* stream);
+/* cast_vector (kernels.cpp:343-360): out = round_out(x / s), s = *scale_dev
+ * when non-NULL else `scale` (must be positive and finite) */
+int mpmg_gpu_cast(int64_t n, const void* x, int32_t x_prec, void* out, int32_t out_prec, const double* scale_dev,
+                  double scale, uint32_t policy, void* stream);
+/* dot_fp64 / norm2_fp64 (kernels.cpp:368-395): sequential fma accumulation in
+ * index order on one device thread -- bitwise the reference's value. */
+int mpmg_gpu_dot_seq(int64_t n, const void* x, int32_t x_prec, const void* y, int32_t y_prec, double* out_dev,
+                     int32_t take_sqrt, void* stream);
+
+/* ---- device memory helpers for FFI hosts (the C++ drop-in layer, ctypes)
+ * All synchronous on the legacy default stream (stream argument NULL of the
+ * kernel entry points). */
+int mpmg_dev_count(void);                                    /* CUDA devices visible */
+void* mpmg_dev_alloc(size_t bytes);                          /* NULL on failure */
+void mpmg_dev_free(void* p);
+int mpmg_dev_h2d(void* dst_dev, const void* src_host, size_t bytes);
+int mpmg_dev_d2h(void* dst_host, const void* src_dev, size_t bytes);
+int mpmg_dev_memset0(void* p, size_t bytes);
+int mpmg_dev_sync(void);
 
 /* The per-level operator of MgHierarchy::build (multigrid.cpp:290-310) for a
  * grid of `nodes` nodes per dimension in precision `prec`: the assembled Q1

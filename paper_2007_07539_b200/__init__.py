@@ -49,11 +49,12 @@ class DivergedError(RuntimeError):
 
 def build(verbose: bool = False) -> str:
     """Compile libmpmg_b200.so for sm_100a (nvcc; no GPU needed)."""
-    out = subprocess.run(["make", "-C", os.path.join(HERE, "csrc"), "-j8"], capture_output=True, text=True)
-    if verbose:
-        print(out.stdout[-4000:], out.stderr[-4000:])
-    if out.returncode != 0:
-        raise RuntimeError("libmpmg_b200 build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+    for sub in ("csrc", "cpp"):  # the sm_100a library, then the C++ drop-in layer over it
+        out = subprocess.run(["make", "-C", os.path.join(HERE, sub), "-j8"], capture_output=True, text=True)
+        if verbose:
+            print(out.stdout[-4000:], out.stderr[-4000:])
+        if out.returncode != 0:
+            raise RuntimeError(f"{sub} build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
     return LIB_PATH
 
 

@@ -97,11 +97,13 @@ int mpmg_gpu_scale_downcast(int32_t dim, int32_t nodes, const double* x, void* o
 }
 
 int mpmg_gpu_partials_len(int32_t dim, int32_t nodes) {
-  const int a = stencil_partials(dim, nodes, MPMG_FP16), b = stencil_partials(dim, nodes, MPMG_FP32);
-  const int c = stencil_partials(dim, nodes, MPMG_FP64), d = norm2_partials(mpmg_padded_len(dim, nodes));
-  int m = a > b ? a : b;
-  m = m > c ? m : c;
-  return m > d ? m : d;
+  int m = norm2_partials(mpmg_padded_len(dim, nodes));
+  for (int lp : {MPMG_FP16, MPMG_FP32, MPMG_FP64})
+    for (bool up : {false, true}) {
+      const int v = stencil_partials(dim, nodes, lp, up);
+      m = m > v ? m : v;
+    }
+  return m;
 }
 
 int mpmg_gpu_norm2_f64(int32_t dim, int32_t nodes, const double* x, double* partials, double* out_dev,
@@ -122,5 +124,48 @@ int mpmg_build_stencil(int32_t dim, int32_t nodes, int32_t prec, uint32_t policy
 }
 
 double mpmg_round_fp16(double x, int32_t ftz) { return round_fp16(x, ftz != 0); }
+
+int mpmg_dev_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void* mpmg_dev_alloc(size_t bytes) {
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, bytes < 16 ? 16 : bytes);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return nullptr;
+  }
+  return p;
+}
+
+void mpmg_dev_free(void* p) {
+  if (p) cudaFree(p);
+}
+
+int mpmg_dev_h2d(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return MPMG_OK;
+  if (!dst || !src) return MPMG_EINVAL;
+  return rc(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+}
+
+int mpmg_dev_d2h(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return MPMG_OK;
+  if (!dst || !src) return MPMG_EINVAL;
+  return rc(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+}
+
+int mpmg_dev_memset0(void* p, size_t bytes) {
+  if (!bytes) return MPMG_OK;
+  if (!p) return MPMG_EINVAL;
+  return rc(cudaMemset(p, 0, bytes));
+}
+
+int mpmg_dev_sync(void) { return rc(cudaDeviceSynchronize()); }
 
 }  // extern "C"

@@ -1,17 +1,22 @@
-// Coarse sub-hierarchy in ONE thread block: every level too small for the
-// streaming kernels (pitch below the warp footprint) runs inside a single
-// persistent CTA — pre-smoothing, defect, restriction (with the DSH rescale),
-// the CG base solve on level 0, prolongation + correction and post-smoothing
-// — separated by __syncthreads instead of kernel launches. This replaces the
-// coarse part of the reference's recursion (cycle_at, multigrid.cpp:362-393)
-// and cg_solve (multigrid.cpp:91-151).
+// Coarse sub-hierarchy in ONE thread-block cluster: every level whose grid
+// is too small to fill the GPU (<= kClusterPoints interior unknowns, i.e.
+// 31^3 / 127^2 and below) runs inside a single persistent cluster launch of
+// up to 16 CTAs -- pre-smoothing, defect, restriction (with the DSH
+// rescale), the CG base solve on level 0, prolongation + correction and
+// post-smoothing -- separated by hardware cluster barriers instead of kernel
+// launches. Levels with <= kCtaPoints unknowns are worked by CTA 0 alone with
+// __syncthreads; the other CTAs wait at the cluster barrier. This replaces
+// the coarse part of the reference's recursion (cycle_at,
+// multigrid.cpp:362-393) and cg_solve (multigrid.cpp:91-151).
 //
-// Arithmetic is the same per-operation rounding as the streaming kernels.
-// Reductions that the reference accumulates sequentially (dot_fp64 /
-// norm2_fp64, kernels.cpp:368-395; the DSH restriction norm,
-// multigrid.cpp:246-250) are done by one thread in the reference's
-// lexicographic order when the level has <= kSeqDot unknowns, so the base
-// solve is bitwise identical to the reference there.
+// Arithmetic is the same per-operation rounding as the streaming kernels
+// (policy as template parameters). Data stays in global memory (L2-resident
+// at these sizes); values written in one step and read by other CTAs in the
+// next are read after a release/acquire cluster barrier + cluster fence.
+// Reductions the reference accumulates sequentially (dot_fp64 / norm2_fp64,
+// kernels.cpp:368-395; the DSH restriction norm, multigrid.cpp:246-250) run
+// on one thread in the reference's lexicographic order, so the base solve is
+// bitwise identical to the reference.
 #include <type_traits>
 
 #include "mpmg_arith.cuh"
@@ -23,47 +28,25 @@ using namespace mpmg_dev;
 
 namespace {
 
-constexpr int kCoarseThreads = 512;
-constexpr long long kSeqDot = 32768;
+constexpr int kThreads = 1024;
+constexpr int kCtaPoints = 4096;
 
 template <int PR> struct T_;
 template <> struct T_<P16> { using T = __half; };
 template <> struct T_<P32> { using T = float; };
 template <> struct T_<P64> { using T = double; };
 
-// Policy is a runtime value here: the coarse kernel is latency-bound, and a
-// single instantiation keeps the build fast.
-struct Pol {
-  bool ftz, fma, acc32;
-};
+// loads of data written earlier in this launch (plain L1-cached loads; see
+// cluster_sync for the coherence argument)
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) { return *p; }
 
-__device__ __forceinline__ __half rfma16(Pol p, __half a, __half b, __half c) {
-  __half r;
-  if (p.fma) r = __hfma(a, b, c);
-  else {
-    __half m = __hmul_rn(a, b);
-    if (p.ftz) m = flush16s(m);
-    r = __hadd_rn(m, c);
-  }
-  return p.ftz ? flush16s(r) : r;
-}
-__device__ __forceinline__ float rfma32(Pol p, float a, float b, float c) {
-  float r;
-  if (p.fma) r = __fmaf_rn(a, b, c);
-  else {
-    float m = __fmul_rn(a, b);
-    if (p.ftz) m = flush32(m);
-    r = __fadd_rn(m, c);
-  }
-  return p.ftz ? flush32(r) : r;
-}
-
-template <int PR>
+template <int PR, bool FTZ, bool FMA, bool ACC32>
 struct Lv {
   using T = typename T_<PR>::T;
-  static __device__ __forceinline__ T from(Pol p, double v) {
-    if constexpr (PR == P16) return p.ftz ? round16<true>(v) : round16<false>(v);
-    else if constexpr (PR == P32) return p.ftz ? round32<true>(v) : round32<false>(v);
+  static __device__ __forceinline__ T from(double v) {
+    if constexpr (PR == P16) return round16<FTZ>(v);
+    else if constexpr (PR == P32) return round32<FTZ>(v);
     else return v;
   }
   static __device__ __forceinline__ double wide(T v) {
@@ -71,263 +54,103 @@ struct Lv {
     else return (double)v;
   }
   static __device__ __forceinline__ T zero() { return T(0); }
-  static __device__ __forceinline__ T fma(Pol p, T a, T b, T c) {
-    if constexpr (PR == P16) return rfma16(p, a, b, c);
-    else if constexpr (PR == P32) return rfma32(p, a, b, c);
-    else return p.fma ? __fma_rn(a, b, c) : __dadd_rn(__dmul_rn(a, b), c);
+  static __device__ __forceinline__ T fma(T a, T b, T c) {
+    if constexpr (PR == P16) return fma16s<FTZ, FMA>(a, b, c);
+    else if constexpr (PR == P32) return fma32<FTZ, FMA>(a, b, c);
+    else return fma64<FMA>(a, b, c);
   }
-  static __device__ __forceinline__ T mul(Pol p, T a, T b) {
-    if constexpr (PR == P16) { const __half m = __hmul_rn(a, b); return p.ftz ? flush16s(m) : m; }
-    else if constexpr (PR == P32) { const float m = __fmul_rn(a, b); return p.ftz ? flush32(m) : m; }
-    else return __dmul_rn(a, b);
+  static __device__ __forceinline__ T mul(T a, T b) {
+    if constexpr (PR == P16) return mul16s<FTZ>(a, b);
+    else if constexpr (PR == P32) return mul32<FTZ>(a, b);
+    else return mul64(a, b);
   }
   // transfer_product step (multigrid.cpp:166-195): FP32 unfused flushes only the sum
-  static __device__ __forceinline__ T xfer(Pol p, double w, T x, T acc) {
-    if constexpr (PR == P32) {
-      const float r = p.fma ? __fmaf_rn((float)w, x, acc) : __fadd_rn(__fmul_rn((float)w, x), acc);
-      return p.ftz ? flush32(r) : r;
-    } else return fma(p, from(p, w), x, acc);
+  static __device__ __forceinline__ T xfer(double w, T x, T acc) {
+    if constexpr (PR == P32) return f32<FTZ>(FMA ? __fmaf_rn((float)w, x, acc) : __fadd_rn(__fmul_rn((float)w, x), acc));
+    else return fma(from(w), x, acc);
   }
-  // A x at padded index i (all 3^dim taps; ghosts are zero)
-  static __device__ __forceinline__ T apply(Pol p, const CoarseLevel& L, const T* x, long long i, int P) {
-    const long long pl = L.dim == 3 ? (long long)P * P : 0;
-    if constexpr (PR == P16) {
-      if (p.acc32) {  // Fp16Accum::FP32 (kernels.cpp:151-162)
-        float acc = 0.0f;
-        int t = 0;
-        for (int dz = (L.dim == 3 ? -1 : 0); dz <= (L.dim == 3 ? 1 : 0); ++dz)
-          for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx, ++t)
-              acc = rfma32(p, (float)L.taps[t], __half2float(x[i + dz * pl + (long long)dy * P + dx]), acc);
-        const __half h = __float2half_rn(acc);
-        return p.ftz ? flush16s(h) : h;
-      }
+  // A x at padded index i (all 3^dim taps; ghosts are zero); x read via L2
+  static __device__ __forceinline__ T apply(const CoarseLevel& L, const T* x, int i, int P) {
+    const int pl = L.dim == 3 ? P * P : 0;
+    if constexpr (PR == P16 && ACC32) {  // Fp16Accum::FP32 (kernels.cpp:151-162)
+      float acc = 0.0f;
+      int t = 0;
+      for (int dz = (L.dim == 3 ? -1 : 0); dz <= (L.dim == 3 ? 1 : 0); ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx, ++t)
+            acc = fma32<FTZ, FMA>((float)L.taps[t], __half2float(ldcg(x + i + dz * pl + dy * P + dx)), acc);
+      return f16s<FTZ>(__float2half_rn(acc));
+    } else {
+      T acc = zero();
+      int t = 0;
+      for (int dz = (L.dim == 3 ? -1 : 0); dz <= (L.dim == 3 ? 1 : 0); ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx, ++t)
+            acc = fma(from(L.taps[t]), ldcg(x + i + dz * pl + dy * P + dx), acc);
+      return acc;
     }
-    T acc = zero();
-    int t = 0;
-    for (int dz = (L.dim == 3 ? -1 : 0); dz <= (L.dim == 3 ? 1 : 0); ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx, ++t)
-          acc = fma(p, from(p, L.taps[t]), x[i + dz * pl + (long long)dy * P + dx], acc);
-    return acc;
   }
 };
 
 struct Pt {
-  long long n;  // interior points
-  int P, dim;
-  __device__ __forceinline__ long long idx(long long k) const {
-    const long long m = P - 1;
-    const long long x = k % m + 1;
-    if (dim == 2) return (k / m + 1) * P + x;
-    return ((k / (m * m) + 1) * P + (k / m) % m + 1) * (long long)P + x;
+  int n, m, P, dim;
+  __device__ __forceinline__ int idx(int k) const {  // compact k -> padded index
+    const int x = k % m + 1;
+    const int q = k / m;
+    if (dim == 2) return (q + 1) * P + x;
+    return ((q / m + 1) * P + q % m + 1) * P + x;
   }
 };
 
 __device__ __forceinline__ Pt points(const CoarseLevel& L) {
   Pt p;
   p.P = L.nodes - 1;
+  p.m = p.P - 1;
   p.dim = L.dim;
-  const long long m = p.P - 1;
-  p.n = L.dim == 3 ? m * m * m : m * m;
+  p.n = L.dim == 3 ? p.m * p.m * p.m : p.m * p.m;
   return p;
 }
 
-// sequential fma dot in lexicographic interior order (kernels.cpp:368-382)
-template <typename TA, typename TB, typename W1, typename W2>
-__device__ double dot_seq(const Pt& p, const TA* x, const TB* y, W1 wx, W2 wy) {
-  double acc = 0.0;
-  for (long long k = 0; k < p.n; ++k) {
-    const long long i = p.idx(k);
-    acc = __fma_rn(wx(x[i]), wy(y[i]), acc);
-  }
-  return acc;
+// release/acquire cluster barrier; the cluster-scope fence invalidates L1
+// so plain (L1-cached) loads see the other CTAs' writes of the last step
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n\t"
+      "fence.acq_rel.cluster;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
 }
 
+template <bool FTZ, bool FMA, bool ACC32>
 struct Coarse {
   const CoarseArgs& a;
-  Pol pol;
-  __device__ Coarse(const CoarseArgs& args, Pol p) : a(args), pol(p) {}
+  unsigned rank, ncta;
+  __device__ Coarse(const CoarseArgs& args) : a(args), rank(cluster_rank()), ncta(cluster_size()) {}
+
+  template <int PR> using O = Lv<PR, FTZ, FMA, ACC32>;
+
+  __device__ bool small(const CoarseLevel& L) const { return points(L).n <= kCtaPoints; }
+  // team of a level: the whole cluster, or CTA 0 alone
+  __device__ bool in_team(const CoarseLevel& L) const { return !small(L) || rank == 0; }
+  __device__ void sync(const CoarseLevel& L) {
+    if (small(L)) __syncthreads();
+    else cluster_sync();
+  }
 
   template <typename F>
   __device__ void for_points(const CoarseLevel& L, F&& f) {
     const Pt p = points(L);
-    for (long long k = threadIdx.x; k < p.n; k += blockDim.x) f(p.idx(k), p.P);
-  }
-
-  template <int PR>
-  __device__ void jacobi(const CoarseLevel& L, const void* bv, const void* uin, void* uout, bool from_zero) {
-    using O = Lv<PR>;
-    using T = typename O::T;
-    const T* b = static_cast<const T*>(bv);
-    const T* u = static_cast<const T*>(uin);
-    T* o = static_cast<T*>(uout);
-    const T w = O::from(pol, L.omega), d = O::from(pol, L.inv_diag), m1 = O::from(pol, -1.0);
-    for_points(L, [&](long long i, int P) {
-      const T t = from_zero ? O::zero() : O::apply(pol, L, u, i, P);
-      const T r = O::fma(pol, m1, t, b[i]);
-      o[i] = O::fma(pol, w, O::mul(pol, d, r), from_zero ? O::zero() : u[i]);
-    });
-  }
-
-  template <int PR>
-  __device__ void defect(const CoarseLevel& L, const void* bv, const void* uv, void* rv) {
-    using O = Lv<PR>;
-    using T = typename O::T;
-    const T m1 = O::from(pol, -1.0);
-    for_points(L, [&](long long i, int P) {
-      static_cast<T*>(rv)[i] = O::fma(pol, m1, O::apply(pol, L, static_cast<const T*>(uv), i, P), static_cast<const T*>(bv)[i]);
-    });
-  }
-
-  // R r_f into C.prod (binary64 value domain of the fine-precision product)
-  template <int FP>
-  __device__ void restrict_prod(const CoarseLevel& F, const CoarseLevel& C, const void* rfv) {
-    using O = Lv<FP>;
-    using T = typename O::T;
-    const T* rf = static_cast<const T*>(rfv);
-    const int Pf = F.nodes - 1;
-    const long long pf = F.dim == 3 ? (long long)Pf * Pf : 0;
-    for_points(C, [&](long long ci, int Pc) {
-      const long long m = Pc;
-      const long long cx = ci % m, cy = (ci / m) % m, cz = F.dim == 3 ? ci / (m * m) : 0;
-      const long long cf = cz * 2 * pf + cy * 2 * Pf + cx * 2;
-      T acc = O::zero();
-      for (int dz = (F.dim == 3 ? -1 : 0); dz <= (F.dim == 3 ? 1 : 0); ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            const double w = (dx == 0 ? 1.0 : 0.5) * (dy == 0 ? 1.0 : 0.5) * (dz == 0 ? 1.0 : 0.5);
-            const T x = rf[cf + dz * pf + (long long)dy * Pf + dx];
-            acc = O::xfer(pol, w, x, acc);
-          }
-      C.prod[ci] = O::wide(acc);
-    });
-  }
-
-  template <int CPc>
-  __device__ void restrict_store(const CoarseLevel& C, double scale) {
-    using O = Lv<CPc>;
-    using T = typename O::T;
-    for_points(C, [&](long long ci, int) { static_cast<T*>(C.b)[ci] = O::from(pol, C.prod[ci] / scale); });
-  }
-
-  // u_f += round_f(scale * P c) (prod in coarse precision)
-  template <int FP, int CPc>
-  __device__ void prolong(const CoarseLevel& F, const CoarseLevel& C, const void* ccv, void* ufv, double scale) {
-    using OC = Lv<CPc>;
-    using OF = Lv<FP>;
-    using TC = typename OC::T;
-    using TF = typename OF::T;
-    const TC* cc = static_cast<const TC*>(ccv);
-    TF* uf = static_cast<TF*>(ufv);
-    const int Pc = C.nodes - 1;
-    for_points(F, [&](long long fi, int Pf) {
-      const long long m = Pf;
-      const int fx = (int)(fi % m), fy = (int)((fi / m) % m), fz = F.dim == 3 ? (int)(fi / (m * m)) : 0;
-      const int nx = (fx & 1) ? 2 : 1, ny = (fy & 1) ? 2 : 1, nz = F.dim == 3 ? ((fz & 1) ? 2 : 1) : 1;
-      const int px[2] = {fx >> 1, (fx + 1) >> 1}, py[2] = {fy >> 1, (fy + 1) >> 1}, pz[2] = {fz >> 1, (fz + 1) >> 1};
-      const double w = ((fx & 1) ? 0.5 : 1.0) * ((fy & 1) ? 0.5 : 1.0) * (F.dim == 3 && (fz & 1) ? 0.5 : 1.0);
-      TC acc = OC::zero();
-      for (int c = 0; c < nz; ++c)
-        for (int b = 0; b < ny; ++b)
-          for (int aa = 0; aa < nx; ++aa) {
-            const long long ci = (F.dim == 3 ? (long long)pz[c] * Pc * Pc : 0) + (long long)py[b] * Pc + px[aa];
-            acc = OC::xfer(pol, w, cc[ci], acc);
-          }
-      const TF t = OF::from(pol, OC::wide(acc) * scale);
-      uf[fi] = OF::fma(pol, OF::from(pol, 1.0), t, uf[fi]);
-    });
-  }
-
-  // CG on level 0 (multigrid.cpp:91-151)
-  template <int PR>
-  __device__ void cg(const CoarseLevel& L, const void* bv, void* uv) {
-    using O = Lv<PR>;
-    using T = typename O::T;
-    __shared__ double sh[4];
-    __shared__ double red[kCoarseThreads];
-    const T* b = static_cast<const T*>(bv);
-    T* u = static_cast<T*>(uv);
-    T* r = static_cast<T*>(a.cg_r);
-    T* p = static_cast<T*>(a.cg_p);
-    T* ap = static_cast<T*>(a.cg_ap);
-    T* sc = static_cast<T*>(a.cg_s);
-    T* best = static_cast<T*>(a.cg_best);
-    const Pt pt = points(L);
-    const auto wd = [](T v) { return O::wide(v); };
-    auto dot = [&](const T* x, const T* y) -> double {
-      // returns the value on thread 0 only; caller broadcasts
-      if (pt.n <= kSeqDot) {
-        if (threadIdx.x == 0) sh[3] = dot_seq(pt, x, y, wd, wd);
-      } else {
-        double acc = 0.0;
-        for (long long k = threadIdx.x; k < pt.n; k += blockDim.x) {
-          const long long i = pt.idx(k);
-          acc = __fma_rn(O::wide(x[i]), O::wide(y[i]), acc);
-        }
-        red[threadIdx.x] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          double s = 0.0;
-          for (int t = 0; t < (int)blockDim.x; ++t) s += red[t];
-          sh[3] = s;
-        }
-      }
-      __syncthreads();
-      const double v = sh[3];
-      __syncthreads();
-      return v;
-    };
-    const int max_it = a.base_maxit > 0 ? a.base_maxit : 10 * (int)pt.n;
-    for_points(L, [&](long long i, int) {
-      u[i] = O::zero();
-      r[i] = b[i];
-      p[i] = b[i];
-      best[i] = O::zero();
-    });
-    __syncthreads();
-    const double norm_b = sqrt(dot(b, b));
-    if (norm_b == 0.0) return;
-    const double thr = a.base_mode == 0 ? a.base_tol * norm_b : a.base_tol;
-    double rz = dot(r, r);
-    double true_res = norm_b, best_res = norm_b;
-    int it = 0;
-    while (true_res >= thr && it < max_it) {
-      for_points(L, [&](long long i, int P) { ap[i] = O::apply(pol, L, p, i, P); });
-      __syncthreads();
-      const double pAp = dot(p, ap);
-      if (!(pAp > 0.0) || !isfinite(pAp)) break;
-      const double alpha = rz / pAp;
-      const T al = O::from(pol, alpha), mal = O::from(pol, -alpha);
-      for_points(L, [&](long long i, int) {
-        u[i] = O::fma(pol, al, p[i], u[i]);
-        r[i] = O::fma(pol, mal, ap[i], r[i]);
-      });
-      __syncthreads();
-      const double rz_new = dot(r, r);
-      ++it;
-      for_points(L, [&](long long i, int P) { sc[i] = O::apply(pol, L, u, i, P); });
-      __syncthreads();
-      const T m1 = O::from(pol, -1.0);
-      for_points(L, [&](long long i, int) { sc[i] = O::fma(pol, m1, sc[i], b[i]); });
-      __syncthreads();
-      true_res = sqrt(dot(sc, sc));
-      if (true_res < best_res) {
-        best_res = true_res;
-        for_points(L, [&](long long i, int) { best[i] = u[i]; });
-        __syncthreads();
-      }
-      if (rz == 0.0) break;
-      const T be = O::from(pol, rz_new / rz);
-      for_points(L, [&](long long i, int) { p[i] = O::fma(pol, be, p[i], r[i]); });
-      __syncthreads();
-      rz = rz_new;
-    }
-    if (true_res > best_res) {
-      for_points(L, [&](long long i, int) { u[i] = best[i]; });
-      __syncthreads();
-    }
-    if (threadIdx.x == 0 && a.cg_iterations) *a.cg_iterations = it;
+    int start = threadIdx.x, stride = blockDim.x;
+    if (!small(L)) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
+    for (int k = start; k < p.n; k += stride) f(p.idx(k), p.P);
   }
 
   template <typename F>
@@ -337,31 +160,202 @@ struct Coarse {
     else f(std::integral_constant<int, P64>{});
   }
 
-  __device__ void copy_level(const CoarseLevel& L, const void* src, void* dst) {
-    const int bytes = mpmg_dev_bytes(L.prec);
-    const Pt p = points(L);
-    for (long long k = threadIdx.x; k < p.n; k += blockDim.x) {
-      const long long i = p.idx(k);
-      if (bytes == 2) static_cast<uint16_t*>(dst)[i] = static_cast<const uint16_t*>(src)[i];
-      else if (bytes == 4) static_cast<uint32_t*>(dst)[i] = static_cast<const uint32_t*>(src)[i];
-      else static_cast<uint64_t*>(dst)[i] = static_cast<const uint64_t*>(src)[i];
-    }
+  template <int PR>
+  __device__ void jacobi(const CoarseLevel& L, const void* bv, const void* uin, void* uout, bool from_zero) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    const T* b = static_cast<const T*>(bv);
+    const T* u = static_cast<const T*>(uin);
+    T* o = static_cast<T*>(uout);
+    const T w = OP::from(L.omega), d = OP::from(L.inv_diag), m1 = OP::from(-1.0);
+    for_points(L, [&](int i, int P) {
+      const T t = from_zero ? OP::zero() : OP::apply(L, u, i, P);
+      const T r = OP::fma(m1, t, ldcg(b + i));
+      o[i] = OP::fma(w, OP::mul(d, r), from_zero ? OP::zero() : ldcg(u + i));
+    });
   }
-  static __device__ __forceinline__ int mpmg_dev_bytes(int prec) { return prec == MPMG_FP16 ? 2 : (prec == MPMG_FP32 ? 4 : 8); }
 
-  // smoothing with ping-pong between L.u and L.u2; returns the buffer that
-  // holds the result. `cur` is the current iterate buffer (or null: zero).
+  template <int PR>
+  __device__ void defect(const CoarseLevel& L, const void* bv, const void* uv, void* rv) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    const T m1 = OP::from(-1.0);
+    for_points(L, [&](int i, int P) {
+      static_cast<T*>(rv)[i] = OP::fma(m1, OP::apply(L, static_cast<const T*>(uv), i, P), ldcg(static_cast<const T*>(bv) + i));
+    });
+  }
+
+  // R r_f (product in the fine precision FP) -> coarse b; when `keep`, the
+  // binary64 products go to C.prod first (DSH rescale norm)
+  template <int FP>
+  __device__ void restrict_to(const CoarseLevel& F, const CoarseLevel& C, const void* rfv, bool keep) {
+    using OF = O<FP>;
+    using T = typename OF::T;
+    const T* rf = static_cast<const T*>(rfv);
+    const int Pf = F.nodes - 1;
+    const int pf = F.dim == 3 ? Pf * Pf : 0;
+    for_points(C, [&](int ci, int Pc) {
+      const int cx = ci % Pc, cy = (ci / Pc) % Pc, cz = F.dim == 3 ? ci / (Pc * Pc) : 0;
+      const int cf = cz * 2 * pf + cy * 2 * Pf + cx * 2;
+      T acc = OF::zero();
+      for (int dz = (F.dim == 3 ? -1 : 0); dz <= (F.dim == 3 ? 1 : 0); ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const double w = (dx == 0 ? 1.0 : 0.5) * (dy == 0 ? 1.0 : 0.5) * (dz == 0 ? 1.0 : 0.5);
+            acc = OF::xfer(w, ldcg(rf + cf + dz * pf + dy * Pf + dx), acc);
+          }
+      if (keep) C.prod[ci] = OF::wide(acc);
+      else by_prec(C.prec, [&](auto cp) {
+        using OC = O<decltype(cp)::value>;
+        static_cast<typename OC::T*>(C.b)[ci] = OC::from(OF::wide(acc));  // scale 1
+      });
+    });
+  }
+
+  template <int CPc>
+  __device__ void restrict_store(const CoarseLevel& C, double scale) {
+    using OC = O<CPc>;
+    for_points(C, [&](int ci, int) {
+      static_cast<typename OC::T*>(C.b)[ci] = OC::from(C.prod[ci] / scale);
+    });
+  }
+
+  // u_f += round_f(scale * P c) (product in the coarse precision)
+  template <int FP, int CPc>
+  __device__ void prolong(const CoarseLevel& F, const CoarseLevel& C, const void* ccv, void* ufv, double scale) {
+    using OC = O<CPc>;
+    using OF = O<FP>;
+    using TC = typename OC::T;
+    using TF = typename OF::T;
+    const TC* cc = static_cast<const TC*>(ccv);
+    TF* uf = static_cast<TF*>(ufv);
+    const int Pc = C.nodes - 1;
+    for_points(F, [&](int fi, int Pf) {
+      const int fx = fi % Pf, fy = (fi / Pf) % Pf, fz = F.dim == 3 ? fi / (Pf * Pf) : 0;
+      const int nx = (fx & 1) ? 2 : 1, ny = (fy & 1) ? 2 : 1, nz = F.dim == 3 ? ((fz & 1) ? 2 : 1) : 1;
+      const int px[2] = {fx >> 1, (fx + 1) >> 1}, py[2] = {fy >> 1, (fy + 1) >> 1}, pz[2] = {fz >> 1, (fz + 1) >> 1};
+      const double w = ((fx & 1) ? 0.5 : 1.0) * ((fy & 1) ? 0.5 : 1.0) * (F.dim == 3 && (fz & 1) ? 0.5 : 1.0);
+      TC acc = OC::zero();
+      for (int c = 0; c < nz; ++c)
+        for (int b = 0; b < ny; ++b)
+          for (int aa = 0; aa < nx; ++aa) {
+            const int ci = (F.dim == 3 ? pz[c] * Pc * Pc : 0) + py[b] * Pc + px[aa];
+            acc = OC::xfer(w, ldcg(cc + ci), acc);
+          }
+      const TF t = OF::from(OC::wide(acc) * scale);
+      uf[fi] = OF::fma(OF::from(1.0), t, ldcg(uf + fi));
+    });
+  }
+
+  // sequential fma dot in lexicographic interior order (kernels.cpp:368-382)
+  template <typename TA, typename TB>
+  __device__ double dot_seq(const Pt& p, const TA* x, const TB* y) {
+    double acc = 0.0;
+    for (int k = 0; k < p.n; ++k) {
+      const int i = p.idx(k);
+      acc = __fma_rn((double)wide_v(ldcg(x + i)), (double)wide_v(ldcg(y + i)), acc);
+    }
+    return acc;
+  }
+  template <typename T>
+  static __device__ __forceinline__ double wide_v(T v) {
+    if constexpr (std::is_same<T, __half>::value) return (double)__half2float(v);
+    else return (double)v;
+  }
+
+  // CG on level 0 (multigrid.cpp:91-151), CTA 0 only
+  template <int PR>
+  __device__ void cg(const CoarseLevel& L, const void* bv, void* uv) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    __shared__ double sh;
+    const T* b = static_cast<const T*>(bv);
+    T* u = static_cast<T*>(uv);
+    T* r = static_cast<T*>(a.cg_r);
+    T* p = static_cast<T*>(a.cg_p);
+    T* ap = static_cast<T*>(a.cg_ap);
+    T* sc = static_cast<T*>(a.cg_s);
+    T* best = static_cast<T*>(a.cg_best);
+    const Pt pt = points(L);
+    auto dot = [&](const T* x, const T* y) -> double {
+      __syncthreads();
+      if (threadIdx.x == 0) sh = dot_seq(pt, x, y);
+      __syncthreads();
+      const double v = sh;
+      __syncthreads();
+      return v;
+    };
+    auto each = [&](auto&& f) {
+      for (int k = threadIdx.x; k < pt.n; k += blockDim.x) f(pt.idx(k));
+      __syncthreads();
+    };
+    const int max_it = a.base_maxit > 0 ? a.base_maxit : 10 * pt.n;
+    each([&](int i) {
+      u[i] = OP::zero();
+      r[i] = ldcg(b + i);
+      p[i] = ldcg(b + i);
+      best[i] = OP::zero();
+    });
+    const double norm_b = sqrt(dot(b, b));
+    if (norm_b == 0.0) return;
+    const double thr = a.base_mode == 0 ? a.base_tol * norm_b : a.base_tol;
+    double rz = dot(r, r);
+    double true_res = norm_b, best_res = norm_b;
+    int it = 0;
+    const T m1 = OP::from(-1.0);
+    while (true_res >= thr && it < max_it) {
+      each([&](int i) { ap[i] = OP::apply(L, p, i, pt.P); });
+      const double pAp = dot(p, ap);
+      if (!(pAp > 0.0) || !isfinite(pAp)) break;
+      const double alpha = rz / pAp;
+      const T al = OP::from(alpha), mal = OP::from(-alpha);
+      each([&](int i) {
+        u[i] = OP::fma(al, ldcg(p + i), ldcg(u + i));
+        r[i] = OP::fma(mal, ldcg(ap + i), ldcg(r + i));
+      });
+      const double rz_new = dot(r, r);
+      ++it;
+      each([&](int i) { sc[i] = OP::apply(L, u, i, pt.P); });
+      each([&](int i) { sc[i] = OP::fma(m1, ldcg(sc + i), ldcg(b + i)); });
+      true_res = sqrt(dot(sc, sc));
+      if (true_res < best_res) {
+        best_res = true_res;
+        each([&](int i) { best[i] = ldcg(u + i); });
+      }
+      if (rz == 0.0) break;
+      const T be = OP::from(rz_new / rz);
+      each([&](int i) { p[i] = OP::fma(be, ldcg(p + i), ldcg(r + i)); });
+      rz = rz_new;
+    }
+    if (true_res > best_res) each([&](int i) { u[i] = ldcg(best + i); });
+    if (threadIdx.x == 0 && a.cg_iterations) *a.cg_iterations = it;
+  }
+
+  __device__ void copy_level(const CoarseLevel& L, const void* src, void* dst) {
+    for_points(L, [&](int i, int) {
+      if (L.prec == MPMG_FP16) static_cast<uint16_t*>(dst)[i] = static_cast<const uint16_t*>(src)[i];
+      else if (L.prec == MPMG_FP32) static_cast<uint32_t*>(dst)[i] = static_cast<const uint32_t*>(src)[i];
+      else static_cast<uint64_t*>(dst)[i] = static_cast<const uint64_t*>(src)[i];
+    });
+  }
+
+  // ping-pong smoothing between L.u and L.u2; returns the result buffer
   __device__ void* smooth(const CoarseLevel& L, void* cur, int steps) {
     for (int s = 0; s < steps; ++s) {
       void* out = (cur == L.u) ? L.u2 : L.u;
       const bool z = cur == nullptr;
-      by_prec(L.prec, [&](auto pc) { jacobi<decltype(pc)::value>(L, L.b, z ? L.b : cur, out, z); });
-      __syncthreads();
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { jacobi<decltype(pc)::value>(L, L.b, z ? L.b : cur, out, z); });
+      sync(L);
       cur = out;
     }
     return cur;
   }
 
+  // Every CTA walks the same schedule; an op on a small level is worked by
+  // CTA 0 only and followed by __syncthreads, an op on a big level by the
+  // whole cluster and followed by a cluster barrier. The one extra cluster
+  // barrier before prolongating a small level's correction into a big level
+  // publishes CTA 0's small-level results.
   __device__ void run() {
     __shared__ double scales[kMaxCoarseLevels];
     void* cur[kMaxCoarseLevels];
@@ -369,61 +363,68 @@ struct Coarse {
     // down-sweep (cycle_at before the recursive call)
     for (int l = top; l >= 1; --l) {
       const CoarseLevel& L = a.lv[l];
+      const CoarseLevel& C = a.lv[l - 1];
       void* u = smooth(L, nullptr, a.pre);
       if (u == nullptr) {  // pre_steps == 0: u = 0
-        for_points(L, [&](long long i, int) {
+        if (in_team(L)) for_points(L, [&](int i, int) {
           if (L.prec == MPMG_FP16) static_cast<uint16_t*>(L.u)[i] = 0;
           else if (L.prec == MPMG_FP32) static_cast<float*>(L.u)[i] = 0.f;
           else static_cast<double*>(L.u)[i] = 0.0;
         });
-        __syncthreads();
+        sync(L);
         u = L.u;
       }
       cur[l] = u;
-      by_prec(L.prec, [&](auto pc) { defect<decltype(pc)::value>(L, L.b, u, L.r); });
-      __syncthreads();
-      const CoarseLevel& C = a.lv[l - 1];
-      by_prec(L.prec, [&](auto pc) { restrict_prod<decltype(pc)::value>(L, C, L.r); });
-      __syncthreads();
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { defect<decltype(pc)::value>(L, L.b, u, L.r); });
+      sync(L);
+      const bool rescale = a.rescale && C.prec == MPMG_FP16;  // multigrid.cpp:383
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { restrict_to<decltype(pc)::value>(L, C, L.r, rescale); });
+      sync(L);
       if (threadIdx.x == 0) {
-        double s = 1.0;
-        if (a.rescale && C.prec == MPMG_FP16) {  // multigrid.cpp:246-250
+        double sc = 1.0;
+        if (rescale && in_team(L)) {  // multigrid.cpp:246-250, sequential fma order
           const Pt pc = points(C);
           double acc = 0.0;
-          for (long long k = 0; k < pc.n; ++k) {
+          for (int k = 0; k < pc.n; ++k) {
             const double v = C.prod[pc.idx(k)];
             acc = __fma_rn(v, v, acc);
           }
           const double nrm = sqrt(acc);
-          if (nrm > 0.0 && isfinite(nrm)) s = nrm;
+          if (nrm > 0.0 && isfinite(nrm)) sc = nrm;
         }
-        scales[l - 1] = s;
+        scales[l - 1] = sc;
       }
       __syncthreads();
-      by_prec(C.prec, [&](auto pc) { restrict_store<decltype(pc)::value>(C, scales[l - 1]); });
-      __syncthreads();
+      if (rescale) {
+        if (in_team(L)) by_prec(C.prec, [&](auto cp) { restrict_store<decltype(cp)::value>(C, scales[l - 1]); });
+        sync(L);
+      }
     }
-    // base solve
+    // base solve on CTA 0
     {
       const CoarseLevel& B = a.lv[0];
-      by_prec(B.prec, [&](auto pc) { cg<decltype(pc)::value>(B, B.b, B.u); });
+      if (rank == 0) by_prec(B.prec, [&](auto pc) { cg<decltype(pc)::value>(B, B.b, B.u); });
       __syncthreads();
+      if (!small(B)) cluster_sync();
       cur[0] = B.u;
     }
     // up-sweep
     for (int l = 1; l <= top; ++l) {
       const CoarseLevel& L = a.lv[l];
       const CoarseLevel& C = a.lv[l - 1];
-      by_prec(L.prec, [&](auto fp) {
-        by_prec(C.prec, [&](auto cp) {
-          prolong<decltype(fp)::value, decltype(cp)::value>(L, C, cur[l - 1], cur[l], scales[l - 1]);
+      if (!small(L) && small(C)) cluster_sync();
+      if (in_team(L)) {
+        by_prec(L.prec, [&](auto fp) {
+          by_prec(C.prec, [&](auto cp) {
+            prolong<decltype(fp)::value, decltype(cp)::value>(L, C, cur[l - 1], cur[l], scales[l - 1]);
+          });
         });
-      });
-      __syncthreads();
+      }
+      sync(L);
       void* u = smooth(L, cur[l], a.post);
-      if (u != L.u) {
-        copy_level(L, u, L.u);
-        __syncthreads();
+      if (l == top && u != L.u) {  // the caller reads the top correction from L.u
+        if (in_team(L)) copy_level(L, u, L.u);
+        sync(L);
         u = L.u;
       }
       cur[l] = u;
@@ -431,17 +432,60 @@ struct Coarse {
   }
 };
 
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse(const __grid_constant__ CoarseArgs a, Pol p) {
-  Coarse c(a, p);
+template <bool FTZ, bool FMA, bool ACC32>
+__global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a) {
+  Coarse<FTZ, FMA, ACC32> c(a);
   c.run();
+}
+
+template <bool FTZ, bool FMA, bool ACC32>
+cudaError_t launch_t(const CoarseArgs& a, cudaStream_t s) {
+  auto kern = k_coarse<FTZ, FMA, ACC32>;
+  // cluster size: 16 CTAs when the top level is big (non-portable size,
+  // falls back to 8), a single CTA otherwise
+  const CoarseLevel& T = a.lv[a.nlev - 1];
+  const int m = T.nodes - 2;
+  const long long n = T.dim == 3 ? (long long)m * m * m : (long long)m * m;
+  static int max_cluster = 0;
+  if (max_cluster == 0) {
+    max_cluster = 8;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(kThreads);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int c = 0;
+      if (cudaOccupancyMaxActiveClusters(&c, kern, &q) == cudaSuccess && c > 0) max_cluster = 16;
+    }
+    cudaGetLastError();
+  }
+  const int csize = n > kCtaPoints ? max_cluster : 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 }  // namespace
 
 cudaError_t launch_coarse_cycle(const CoarseArgs& a, uint32_t policy, cudaStream_t s) {
-  const Pol p{(policy & MPMG_FTZ) != 0, (policy & MPMG_FMA) != 0, (policy & MPMG_ACC32) != 0};
-  k_coarse<<<1, kCoarseThreads, 0, s>>>(a, p);
-  return cudaGetLastError();
+  const bool ftz = policy & MPMG_FTZ, fma = policy & MPMG_FMA, acc = policy & MPMG_ACC32;
+  if (ftz) {
+    if (fma) return acc ? launch_t<true, true, true>(a, s) : launch_t<true, true, false>(a, s);
+    return acc ? launch_t<true, false, true>(a, s) : launch_t<true, false, false>(a, s);
+  }
+  if (fma) return acc ? launch_t<false, true, true>(a, s) : launch_t<false, true, false>(a, s);
+  return acc ? launch_t<false, false, true>(a, s) : launch_t<false, false, false>(a, s);
 }
 
 }  // namespace mpmg_impl

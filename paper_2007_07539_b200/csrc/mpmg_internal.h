@@ -37,8 +37,22 @@ cudaError_t launch_defect64(const mpmg_stencil& A64, const double* b, const doub
                             bool fma, bool resnorm, cudaStream_t s, const int* gate = nullptr);
 cudaError_t launch_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
                              const double* alpha_dev, double* partials, bool fma, cudaStream_t s);
-// number of partial sums the stencil kernels write for a grid (any LP)
-int stencil_partials(int dim, int nodes, int lp);
+// number of partial sums one launch writes: the fused update with operand
+// precision lp (update = true), or the FP64 defect / residual norm
+int stencil_partials(int dim, int nodes, int lp, bool update);
+// TMA-staged plane kernels (mpmg_plane_*.cu): return false when the shape
+// or policy is not covered (the caller then uses the streaming kernels)
+bool plane_level_op_f16(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                        uint32_t policy, cudaStream_t s, cudaError_t* err);
+bool plane_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                        uint32_t policy, cudaStream_t s, cudaError_t* err);
+bool plane_level_op_f64(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                        uint32_t policy, cudaStream_t s, cudaError_t* err);
+bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
+                    bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err);
+bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
+                     const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err);
+int plane_partials(int dim, int nodes, int lp, bool update);
 // true when the streaming stencil kernels support this level shape
 bool stencil_supported(int dim, int nodes, int prec);
 

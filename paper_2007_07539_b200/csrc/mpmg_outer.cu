@@ -7,6 +7,8 @@ namespace mpmg_impl {
 
 cudaError_t launch_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
                             bool fma, bool resnorm, cudaStream_t s, const int* gate) {
+  cudaError_t pe = cudaSuccess;
+  if (plane_defect64(A64, b, u, r, partials, fma, resnorm, s, gate, &pe)) return pe;
   StencilArgs a = make_args(A64, Geo<P64, P64>::ZC);
   a.x = u; a.b = b; a.out = r; a.partials = partials; a.gate = gate;
   using I2 = std::integral_constant<int, 2>;
@@ -22,6 +24,8 @@ cudaError_t launch_defect64(const mpmg_stencil& A64, const double* b, const doub
 
 cudaError_t launch_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
                              const double* alpha_dev, double* partials, bool fma, cudaStream_t s) {
+  cudaError_t pe = cudaSuccess;
+  if (plane_update_rc(A64, c, c_prec, r, u, alpha_dev, partials, fma, s, &pe)) return pe;
   using I2 = std::integral_constant<int, 2>;
   using I3 = std::integral_constant<int, 3>;
   auto go = [&](auto dimc, auto lpc, auto fmc) -> cudaError_t {
@@ -46,9 +50,12 @@ cudaError_t launch_update_rc(const mpmg_stencil& A64, const void* c, int c_prec,
 
 // partial sums written by the FP64-epilogue kernels (update: stencil operand
 // in precision lp; defect64/resnorm: lp == FP64)
-int stencil_partials(int dim, int nodes, int lp) {
+int stencil_partials(int dim, int nodes, int lp, bool update) {
+  const int pp = plane_partials(dim, nodes, lp, update);
+  if (pp > 0) return pp;
   const int P = pitch(nodes);
   dim3 g;
+  if (!update) lp = MPMG_FP64;
   switch (lp) {
     case MPMG_FP16: { using G = Geo<P16, P64>; g = stencil_grid(dim, P, G::W, G::RY, G::BW, G::ZC); break; }
     case MPMG_FP32: { using G = Geo<P32, P64>; g = stencil_grid(dim, P, G::W, G::RY, G::BW, G::ZC); break; }

@@ -1,0 +1,9 @@
+// TMA-staged plane-kernel instantiations for binary32 levels (mpmg_plane.cuh).
+#include "mpmg_plane_launch.cuh"
+
+namespace mpmg_impl {
+bool plane_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                       uint32_t policy, cudaStream_t s, cudaError_t* err) {
+  return plane_level_op<mpmg_dev::P32>(op, A, x, b, out, omega, policy, s, err);
+}
+}  // namespace mpmg_impl

@@ -1,0 +1,143 @@
+// Host launchers of the TMA-staged plane kernels (mpmg_plane.cuh). Included
+// by one translation unit per operand precision so the instantiations
+// compile in parallel.
+#pragma once
+
+#include <type_traits>
+
+#include "mpmg_internal.h"
+#include "mpmg_plane.cuh"
+
+namespace mpmg_impl {
+
+using namespace mpmg_dev;
+
+// CTA shape per (operand precision, compute precision, op, pitch)
+template <int LP, int CP, int OP, int P>
+struct PlaneCfg {
+  static constexpr int W = P >= 256 ? 8 : P / 32;
+  static constexpr int WX = P / (32 * W);
+  static constexpr bool kWide = CP == P64 || (CP == P32 && LP != P16) || OP == POP_UPDATE;
+  // output rows per thread and warp-rows per CTA
+  static constexpr int RY = kWide ? 2 : 4;
+  static constexpr int WY = WX >= 4 ? 1 : (WX == 2 ? 2 : 4);
+  static constexpr int NS = kWide && W == 8 ? 3 : 4;
+};
+
+inline __half2 h2_of(double v) {
+  const __half h = __double2half(v);
+  return __halves2half2(h, h);
+}
+
+inline PlaneArgs plane_args(const mpmg_stencil& A) {
+  PlaneArgs a{};
+  a.P = pitch(A.nodes);
+  a.plane = (long long)a.P * a.P;
+  for (int i = 0; i < 27; ++i) {
+    const double t = i < A.ntaps ? A.taps[i] : 0.0;
+    a.t16[i] = h2_of(t);
+    a.t32[i] = (float)t;
+    a.t64[i] = t;
+  }
+  a.d16 = h2_of(A.inv_diag);
+  a.d32 = (float)A.inv_diag;
+  a.d64 = A.inv_diag;
+  return a;
+}
+
+// number of SMs of the current device (cached)
+int plane_num_sms();
+
+template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, int P>
+struct PlaneLaunch {
+  using C = PlaneCfg<LP, CP, OP, P>;
+  static constexpr bool SKIPF = CP == P16;
+  using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS>;
+  static constexpr auto kernel = k_plane<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS>;
+
+  // grid: y-tiles x z-chunks, z-chunks sized so the grid is about one wave
+  static dim3 grid(int* zc) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem);
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, K::kThreads, K::kSmem);
+      per_sm = n > 0 ? n : 1;
+    }
+    const int ytiles = (P - 1 + K::TY - 1) / K::TY;
+    const int cap = per_sm * plane_num_sms();
+    int chunks = cap / ytiles;
+    if (chunks < 1) chunks = 1;
+    if (chunks > P - 1) chunks = P - 1;
+    int z = (P - 1 + chunks - 1) / chunks;
+    // small grids are latency-bound: as many CTAs as possible; large grids
+    // keep >= 2 planes per chunk so the z-halo re-reads stay small
+    const int zmin = P >= 256 ? 2 : 1;
+    if (z < zmin) z = zmin;
+    *zc = z;
+    return dim3(ytiles, (P - 1 + z - 1) / z, 1);
+  }
+
+  static cudaError_t run(PlaneArgs a, cudaStream_t s) {
+    int zc = 0;
+    const dim3 g = grid(&zc);
+    a.zc = zc;
+    a.ty = K::TY;
+    kernel<<<g, K::kThreads, K::kSmem, s>>>(a);
+    return cudaGetLastError();
+  }
+
+  static int partials() {
+    int zc = 0;
+    const dim3 g = grid(&zc);
+    return (int)(g.x * g.y);
+  }
+};
+
+// dispatch on the pitch; returns false when the plane kernels do not cover P
+template <typename F>
+inline bool with_pitch(int P, F&& f) {
+  switch (P) {
+    case 32: f(std::integral_constant<int, 32>{}); return true;
+    case 64: f(std::integral_constant<int, 64>{}); return true;
+    case 128: f(std::integral_constant<int, 128>{}); return true;
+    case 256: f(std::integral_constant<int, 256>{}); return true;
+    case 512: f(std::integral_constant<int, 512>{}); return true;
+    case 1024: f(std::integral_constant<int, 1024>{}); return true;
+    default: return false;
+  }
+}
+
+inline bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
+// FP16 stencils may drop the six face taps only when they are exactly zero
+inline bool faces_zero16(const mpmg_stencil& A) {
+  const int f[6] = {4, 10, 12, 14, 16, 22};
+  for (int i : f)
+    if (__half2float(__double2half(A.taps[i])) != 0.0f) return false;
+  return true;
+}
+
+// level op (DEFECT / JACOBI) through the plane kernels; false if not covered
+template <int LP>
+bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                    uint32_t policy, cudaStream_t s, cudaError_t* err) {
+  if (A.dim != 3 || (op != 1 && op != 2)) return false;
+  if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
+  if (LP == P16 && !faces_zero16(A)) return false;
+  if (!aligned16(x) || !aligned16(b) || !aligned16(out)) return false;
+  PlaneArgs a = plane_args(A);
+  a.x = x; a.b = b; a.out = out;
+  const bool ftz = policy & MPMG_FTZ;
+  const double w = round_to(omega, LP, ftz);
+  a.w16 = h2_of(w); a.w32 = (float)w; a.w64 = w;
+  return with_pitch(a.P, [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    if (op == 1) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_DEFECT, true, true, PP>::run(a, s)
+                            : PlaneLaunch<LP, LP, LP, POP_DEFECT, false, true, PP>::run(a, s);
+    else *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP>::run(a, s)
+                    : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP>::run(a, s);
+  });
+}
+
+}  // namespace mpmg_impl

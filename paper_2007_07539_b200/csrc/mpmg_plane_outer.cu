@@ -1,0 +1,79 @@
+// TMA-staged plane kernels of the outer FP64 refinement (ir_solver.cpp:
+// 51-127): FP64 defect (+ ||r||^2 partials), final residual norm, and the
+// fused update u += a c, r -= a A c with c widened from the finest level
+// precision (kernels.cpp:300-341).
+#include <cuda_runtime.h>
+
+#include "mpmg_plane_launch.cuh"
+
+namespace mpmg_impl {
+
+int plane_num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+bool plane_outer_supported(int dim, int nodes) {
+  if (dim != 3) return false;
+  return with_pitch(pitch(nodes), [](auto) {});
+}
+
+bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
+                    bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err) {
+  if (!plane_outer_supported(A64.dim, A64.nodes) || !aligned16(b) || !aligned16(u) || !aligned16(r)) return false;
+  PlaneArgs a = plane_args(A64);
+  a.x = u; a.b = b; a.out = r; a.partials = partials; a.gate = gate;
+  return with_pitch(a.P, [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    if (resnorm) *err = PlaneLaunch<P64, P64, P64, POP_RESNORM, false, true, PP>::run(a, s);  // ir_solver.cpp:38
+    else if (fma) *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::run(a, s);
+    else *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, false, PP>::run(a, s);
+  });
+}
+
+bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
+                     const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err) {
+  if (!plane_outer_supported(A64.dim, A64.nodes) || !aligned16(c) || !aligned16(r) || !aligned16(u)) return false;
+  PlaneArgs a = plane_args(A64);
+  a.x = c; a.r64 = r; a.u64 = u; a.alpha = alpha_dev; a.partials = partials;
+  return with_pitch(a.P, [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    auto go = [&](auto lpc) {
+      constexpr int L = decltype(lpc)::value;
+      *err = fma ? PlaneLaunch<L, P64, P64, POP_UPDATE, false, true, PP>::run(a, s)
+                 : PlaneLaunch<L, P64, P64, POP_UPDATE, false, false, PP>::run(a, s);
+    };
+    switch (c_prec) {
+      case MPMG_FP16: go(std::integral_constant<int, P16>{}); break;
+      case MPMG_FP32: go(std::integral_constant<int, P32>{}); break;
+      default: go(std::integral_constant<int, P64>{}); break;
+    }
+  });
+}
+
+// partial sums written per launch: UPDATE with operand precision lp, or the
+// FP64 defect / residual norm (lp == FP64); -1 when not covered
+// (FMA on/off and DEFECT64/RESNORM instantiations share the shared-memory
+// footprint, hence the occupancy and the grid)
+int plane_partials(int dim, int nodes, int lp, bool update) {
+  if (!plane_outer_supported(dim, nodes)) return -1;
+  int n = -1;
+  with_pitch(pitch(nodes), [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    if (!update) { n = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::partials(); return; }
+    switch (lp) {
+      case MPMG_FP16: n = PlaneLaunch<P16, P64, P64, POP_UPDATE, false, true, PP>::partials(); break;
+      case MPMG_FP32: n = PlaneLaunch<P32, P64, P64, POP_UPDATE, false, true, PP>::partials(); break;
+      default: n = PlaneLaunch<P64, P64, P64, POP_UPDATE, false, true, PP>::partials(); break;
+    }
+  });
+  return n;
+}
+
+}  // namespace mpmg_impl

@@ -18,6 +18,14 @@ namespace {
 
 constexpr int kThreads = 256;
 
+inline bool aligned64(const void* p) { return ((uintptr_t)p & 63u) == 0; }
+
+// one thread per 8 values, at most ~8 waves of 256-thread CTAs per SM
+inline unsigned grid8(size_t len) {
+  const size_t groups = len / 8 + 1;
+  return (unsigned)std::max<size_t>(1, std::min<size_t>((groups + kThreads - 1) / kThreads, 148u * 64u));
+}
+
 inline unsigned blocks_for(size_t n, int per_thread = 1) {
   const size_t t = (n + (size_t)per_thread - 1) / per_thread;
   return (unsigned)std::max<size_t>(1, (t + kThreads - 1) / kThreads);
@@ -178,6 +186,162 @@ __global__ void k_downcast(const double* __restrict__ x, void* __restrict__ out,
     static_cast<typename St<PREC>::T*>(out)[i] = store_round<PREC, FTZ>(__ddiv_rn(x[i], s));
 }
 
+// ---- vectorized forms: 8 consecutive values per thread (16-byte binary16 /
+// 32-byte binary32 / 64-byte binary64 accesses); same arithmetic as above.
+template <int PREC> struct V8;
+template <> struct V8<P16> {
+  __half2 h[4];
+  __device__ __forceinline__ void load(const void* p, long long i) {
+    const uint4 q = *reinterpret_cast<const uint4*>(static_cast<const __half*>(p) + i);
+    h[0] = u2h(q.x); h[1] = u2h(q.y); h[2] = u2h(q.z); h[3] = u2h(q.w);
+  }
+  __device__ __forceinline__ void store(void* p, long long i) const {
+    *reinterpret_cast<uint4*>(static_cast<__half*>(p) + i) = make_uint4(h2u(h[0]), h2u(h[1]), h2u(h[2]), h2u(h[3]));
+  }
+  __device__ __forceinline__ __half get(int e) const { return e & 1 ? __high2half(h[e >> 1]) : __low2half(h[e >> 1]); }
+  __device__ __forceinline__ void set(int e, __half v) {
+    h[e >> 1] = e & 1 ? __halves2half2(__low2half(h[e >> 1]), v) : __halves2half2(v, __high2half(h[e >> 1]));
+  }
+};
+template <> struct V8<P32> {
+  float v[8];
+  __device__ __forceinline__ void load(const void* p, long long i) {
+    const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(p) + i);
+    const float4 a = q[0], b = q[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ __forceinline__ void store(void* p, long long i) const {
+    float4* q = reinterpret_cast<float4*>(static_cast<float*>(p) + i);
+    q[0] = make_float4(v[0], v[1], v[2], v[3]);
+    q[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+  __device__ __forceinline__ float get(int e) const { return v[e]; }
+  __device__ __forceinline__ void set(int e, float x) { v[e] = x; }
+};
+template <> struct V8<P64> {
+  double v[8];
+  __device__ __forceinline__ void load(const void* p, long long i) {
+    const double2* q = reinterpret_cast<const double2*>(static_cast<const double*>(p) + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { const double2 a = q[k]; v[2 * k] = a.x; v[2 * k + 1] = a.y; }
+  }
+  __device__ __forceinline__ void store(void* p, long long i) const {
+    double2* q = reinterpret_cast<double2*>(static_cast<double*>(p) + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = make_double2(v[2 * k], v[2 * k + 1]);
+  }
+  __device__ __forceinline__ double get(int e) const { return v[e]; }
+  __device__ __forceinline__ void set(int e, double x) { v[e] = x; }
+};
+
+// downcast of n8 groups of 8 values (len - 8*n8 tail done by block 0)
+template <int PREC, bool FTZ>
+__global__ void k_downcast8(const double* __restrict__ x, void* __restrict__ out, long long len,
+                            const double* alpha, int scale_enabled) {
+  const double a = *alpha;
+  const double s = (scale_enabled && a > 0.0) ? a : 1.0;
+  const long long n8 = len / 8;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n8; g += (long long)gridDim.x * blockDim.x) {
+    V8<P64> in;
+    in.load(x, 8 * g);
+    V8<PREC> o;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o.set(e, store_round<PREC, FTZ>(__ddiv_rn(in.get(e), s)));
+    o.store(out, 8 * g);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < len - 8 * n8) {
+    const long long i = 8 * n8 + threadIdx.x;
+    static_cast<typename St<PREC>::T*>(out)[i] = store_round<PREC, FTZ>(__ddiv_rn(x[i], s));
+  }
+}
+
+template <int PREC, bool FTZ, bool FMA>
+__device__ __forceinline__ typename St<PREC>::T jz_one(typename St<PREC>::T b, double w, double d) {
+  if constexpr (PREC == P16) {
+    const __half t = mul16s<FTZ>(__double2half(d), b);
+    return fma16s<FTZ, FMA>(__double2half(w), t, __ushort_as_half((unsigned short)0));
+  } else if constexpr (PREC == P32) {
+    return fma32<FTZ, FMA>((float)w, mul32<FTZ>((float)d, b), 0.0f);
+  } else {
+    return fma64<FMA>(w, mul64(d, b), 0.0);
+  }
+}
+
+template <int PREC, bool FTZ, bool FMA>
+__global__ void k_jacobi_zero8(const void* __restrict__ bv, void* __restrict__ uv, long long len, double w, double d) {
+  const long long n8 = len / 8;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n8; g += (long long)gridDim.x * blockDim.x) {
+    V8<PREC> b;
+    b.load(bv, 8 * g);
+    V8<PREC> u;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) u.set(e, jz_one<PREC, FTZ, FMA>(b.get(e), w, d));
+    u.store(uv, 8 * g);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < len - 8 * n8) {
+    const long long i = 8 * n8 + threadIdx.x;
+    using T = typename St<PREC>::T;
+    static_cast<T*>(uv)[i] = jz_one<PREC, FTZ, FMA>(static_cast<const T*>(bv)[i], w, d);
+  }
+}
+
+// prolongation + correction, 8 consecutive fine x per thread (Pf % 8 == 0);
+// same parent order and rounding as k_prolong
+template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
+__global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_, int Pf, const double* scale_dev) {
+  using X = Xfer<CPc, FTZ, FMA>;
+  using TC = typename X::T;
+  const TC* cc = static_cast<const TC*>(cc_);
+  const int groups = Pf / 8;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups * (Pf - 1)) return;
+  const int fy = g / groups + 1;
+  const int x0 = (g % groups) * 8;
+  const int fz = DIM == 3 ? (int)blockIdx.y + 1 : 0;
+  const int Pc = Pf / 2;
+  const int ny = (fy & 1) ? 2 : 1, nz = DIM == 3 ? ((fz & 1) ? 2 : 1) : 1;
+  const int py[2] = {fy >> 1, (fy + 1) >> 1};
+  const int pz[2] = {fz >> 1, (fz + 1) >> 1};
+  const double wy = (fy & 1) ? 0.5 : 1.0, wz = DIM == 3 ? ((fz & 1) ? 0.5 : 1.0) : 1.0;
+  // coarse values x0/2 .. x0/2+4 of each parent row
+  TC c[2][2][5];
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (k < nz && j < ny) {
+        const long long base = (DIM == 3 ? (long long)pz[k] * Pc * Pc : 0) + (long long)py[j] * Pc + x0 / 2;
+#pragma unroll
+        for (int e = 0; e < 5; ++e) c[k][j][e] = (x0 / 2 + e <= Pc) ? __ldg(cc + base + e) : X::zero();
+      }
+    }
+  const double s = scale_dev ? *scale_dev : 1.0;
+  const long long fi = (DIM == 3 ? (long long)fz * Pf * Pf : 0) + (long long)fy * Pf + x0;
+  V8<FP> u;
+  u.load(uf_, fi);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int fx = x0 + e;
+    if (fx == 0) continue;  // ghost node stays zero
+    const int nx = (fx & 1) ? 2 : 1;
+    const double wx = (fx & 1) ? 0.5 : 1.0;
+    const int px0 = (fx >> 1) - x0 / 2;
+    TC acc = X::zero();
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          if (k < nz && j < ny && a < nx) acc = X::step(wx * wy * wz, c[k][j][px0 + a], acc);
+    const auto t = store_round<FP, FTZ>(X::wide(acc) * s);
+    if constexpr (FP == P16) u.set(e, fma16s<FTZ, FMA>(__ushort_as_half((unsigned short)0x3C00), t, u.get(e)));
+    else if constexpr (FP == P32) u.set(e, fma32<FTZ, FMA>(1.0f, t, u.get(e)));
+    else u.set(e, fma64<FMA>(1.0, t, u.get(e)));
+  }
+  u.store(uf_, fi);
+}
+
 // deterministic per-block partial sums of x_i^2 (fixed grid, fixed order)
 __global__ void k_sumsq(const double* __restrict__ x, long long len, double* partials) {
   __shared__ double red[kThreads / 32];
@@ -260,10 +424,15 @@ cudaError_t launch_pack(int dim, int nodes, int prec, const void* compact, void*
 cudaError_t launch_jacobi_zero(int dim, int nodes, int prec, const void* b, void* u, double omega_r,
                                double invdiag_r, uint32_t policy, cudaStream_t s) {
   const size_t len = mpmg_padded_len(dim, nodes);
+  const bool vec = aligned64(b) && aligned64(u);
   return with_prec(prec, [&](auto pc) -> cudaError_t {
     return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
-      k_jacobi_zero<decltype(pc)::value, decltype(ft)::value, decltype(fm)::value>
-          <<<blocks_for(len), kThreads, 0, s>>>(b, u, (long long)len, omega_r, invdiag_r);
+      constexpr int PR = decltype(pc)::value;
+      constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
+      if (vec)
+        k_jacobi_zero8<PR, T, M><<<grid8(len), kThreads, 0, s>>>(b, u, (long long)len, omega_r, invdiag_r);
+      else
+        k_jacobi_zero<PR, T, M><<<blocks_for(len), kThreads, 0, s>>>(b, u, (long long)len, omega_r, invdiag_r);
       return cudaGetLastError();
     });
   });
@@ -293,12 +462,17 @@ cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_pr
   const int Pf = pitch(fine_nodes);
   const dim3 block(32, 8);
   const dim3 grid((Pf - 1 + 31) / 32, (Pf - 1 + 7) / 8, dim == 3 ? Pf - 1 : 1);
+  const bool vec = Pf % 8 == 0 && aligned64(u_fine);
+  const dim3 grid8v((unsigned)(((Pf / 8) * (Pf - 1) + kThreads - 1) / kThreads), dim == 3 ? Pf - 1 : 1);
   return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
     return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
       return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
         constexpr int F = decltype(fp)::value, Cc = decltype(cp)::value;
         constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
-        if (dim == 3) k_prolong<3, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
+        if (vec) {
+          if (dim == 3) k_prolong8<3, F, Cc, T, M><<<grid8v, kThreads, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
+          else k_prolong8<2, F, Cc, T, M><<<grid8v, kThreads, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
+        } else if (dim == 3) k_prolong<3, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
         else k_prolong<2, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
         return cudaGetLastError();
       });
@@ -310,6 +484,16 @@ cudaError_t launch_downcast(int dim, int nodes, const double* x, void* out, int 
                             int scale_enabled, uint32_t policy, cudaStream_t s) {
   const size_t len = mpmg_padded_len(dim, nodes);
   const unsigned blocks = std::min<unsigned>(blocks_for(len, 4), 148u * 16u);
+  if (aligned64(x) && aligned64(out))
+    return with_prec(prec, [&](auto pc) -> cudaError_t {
+      if (policy & MPMG_FTZ)
+        k_downcast8<decltype(pc)::value, true><<<grid8(len), kThreads, 0, s>>>(x, out, (long long)len, alpha_dev,
+                                                                              scale_enabled);
+      else
+        k_downcast8<decltype(pc)::value, false><<<grid8(len), kThreads, 0, s>>>(x, out, (long long)len, alpha_dev,
+                                                                               scale_enabled);
+      return cudaGetLastError();
+    });
   return with_prec(prec, [&](auto pc) -> cudaError_t {
     if (policy & MPMG_FTZ)
       k_downcast<decltype(pc)::value, true><<<blocks, kThreads, 0, s>>>(x, out, (long long)len, alpha_dev, scale_enabled);

@@ -3,9 +3,9 @@
 // v_cycle, multigrid.cpp:282-393, and ir_solve, ir_solver.cpp:51-127),
 // re-designed for one B200:
 //   * every level vector lives in HBM in the ghost-aliased pitch layout;
-//   * a level with a pitch of at least kBigPitch runs the streaming stencil
-//     kernels; all coarser levels (and the CG base solve) run inside one
-//     single-CTA kernel;
+//   * a level with more than kClusterPoints unknowns runs the streaming
+//     stencil kernels; all coarser levels (and the CG base solve) run inside
+//     one thread-block-cluster kernel (mpmg_coarse.cu);
 //   * the outer loop runs on the device: a control kernel reduces ||r||,
 //     applies the reference's stopping rules and sets the condition of a CUDA
 //     graph WHILE node, so a whole solve is one graph launch with no host
@@ -31,7 +31,9 @@ int set_cuda_error(cudaError_t e) {
 
 namespace {
 
-constexpr int kBigPitch = 64;
+// levels with more interior unknowns than this run the streaming (plane)
+// kernels, one launch per operation; the rest run in the coarse cluster kernel
+constexpr long long kClusterPoints = 32768;
 constexpr int kCtlThreads = 256;
 
 struct Level {
@@ -416,7 +418,7 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
     L.omega_r = round_to(c.omega, prec, ftz);
     L.len = mpmg_padded_len(c.dim, nl);
     L.bytes = mpmg_bytes_per_value(prec);
-    L.big = pitch(nl) >= kBigPitch && stencil_supported(c.dim, nl, prec);
+    L.big = (long long)mpmg_interior_len(c.dim, nl) > kClusterPoints && stencil_supported(c.dim, nl, prec);
   }
   // big levels must be a suffix (finest levels)
   for (int l = c.levels - 1; l >= 1; --l)
@@ -451,8 +453,8 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
   S->rlow = S->lv[F].b;
   (void)fprec;
   // partial-sum buffers
-  S->nU = stencil_partials(c.dim, c.nodes, fprec);
-  S->nD = stencil_partials(c.dim, c.nodes, MPMG_FP64);
+  S->nU = stencil_partials(c.dim, c.nodes, fprec, true);
+  S->nD = stencil_partials(c.dim, c.nodes, MPMG_FP64, false);
   const int npart = std::max({S->nU, S->nD, norm2_partials(S->lv[F].len)});
   if (e == cudaSuccess) e = S->alloc(&S->partU, (size_t)npart * 8);
   if (e == cudaSuccess) e = S->alloc(&S->partD, (size_t)npart * 8);
@@ -685,20 +687,20 @@ int mpmg_solver_level_op(mpmg_solver* S, int op, int l, const double* in0, const
     case MPMG_OP_SPMV:
       e = upload_values(S, dim, nodes, prec, in0, L.u);
       if (e == cudaSuccess) {
-        if (L.big) e = launch_level_op(0, L.A, L.u, nullptr, L.r, S->cfg.omega, S->policy(), q);
+        if (stencil_supported(dim, nodes, prec)) e = launch_level_op(0, L.A, L.u, nullptr, L.r, S->cfg.omega, S->policy(), q);
         else return MPMG_EUNSUPPORTED;
       }
       if (e == cudaSuccess) e = download_values(S, dim, nodes, prec, L.r, out);
       break;
     case MPMG_OP_DEFECT:
-      if (!L.big) return MPMG_EUNSUPPORTED;
+      if (!stencil_supported(dim, nodes, prec)) return MPMG_EUNSUPPORTED;
       e = upload_values(S, dim, nodes, prec, in0, L.u);
       if (e == cudaSuccess) e = upload_values(S, dim, nodes, prec, in1, L.b);
       if (e == cudaSuccess) e = launch_level_op(1, L.A, L.u, L.b, L.r, S->cfg.omega, S->policy(), q);
       if (e == cudaSuccess) e = download_values(S, dim, nodes, prec, L.r, out);
       break;
     case MPMG_OP_JACOBI: {
-      if (!L.big) return MPMG_EUNSUPPORTED;
+      if (!stencil_supported(dim, nodes, prec)) return MPMG_EUNSUPPORTED;
       e = upload_values(S, dim, nodes, prec, in1, L.b);
       void* cur = nullptr;
       if (e == cudaSuccess && in0) { e = upload_values(S, dim, nodes, prec, in0, L.u); cur = L.u; }

@@ -56,6 +56,14 @@ inline cudaError_t with_policy(uint32_t policy, F&& f) {
 template <int LP>
 cudaError_t level_op_impl(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                           uint32_t policy, cudaStream_t s) {
+  {  // TMA-staged plane kernels first (3D, pitch a multiple of 32)
+    cudaError_t pe = cudaSuccess;
+    bool done = false;
+    if constexpr (LP == P16) done = plane_level_op_f16(op, A, x, b, out, omega, policy, s, &pe);
+    else if constexpr (LP == P32) done = plane_level_op_f32(op, A, x, b, out, omega, policy, s, &pe);
+    else done = plane_level_op_f64(op, A, x, b, out, omega, policy, s, &pe);
+    if (done) return pe;
+  }
   StencilArgs a = make_args(A, Geo<LP, LP>::ZC);
   a.x = x; a.b = b; a.out = out;
   const bool ftz = policy & MPMG_FTZ;
