@@ -70,6 +70,23 @@ typedef struct mpmg_stencil {
   double inv_diag;  /* Jacobi D^-1 (per-level constant), rounded to prec */
 } mpmg_stencil;
 
+/* A z-slab of a 3D level (multi-GPU slab decomposition): the
+ * rank owns global interior planes z_lo .. z_lo+nz-1, stored as local planes
+ * 1..nz of a slab array in the padded layout with one halo plane on each
+ * side: local plane 0 = global z_lo-1, local plane nz+1 = global z_lo+nz.
+ * A halo plane holds the neighbour's plane (halo_* = 1) or, at the domain
+ * boundary, the zero Dirichlet ghost (halo_* = 0, never read). Allocation:
+ * mpmg_slab_len values. A whole level is the slab {P-1, 1, 0, 0}. */
+typedef struct mpmg_slab {
+  int32_t nz;
+  int32_t z_lo;
+  int32_t halo_lo;
+  int32_t halo_hi;
+} mpmg_slab;
+
+/* (nz + 2) P^2 + P + 1 */
+size_t mpmg_slab_len(int32_t nodes, int32_t nz);
+
 /* Number of values of a padded level vector. */
 size_t mpmg_padded_len(int32_t dim, int32_t nodes);
 /* Number of interior unknowns ((n-2)^dim). */
@@ -137,6 +154,39 @@ int mpmg_gpu_partials_len(int32_t dim, int32_t nodes);
 int mpmg_gpu_norm2_f64(int32_t dim, int32_t nodes, const double* x, double* partials, double* out_dev,
                        void* stream);
 int mpmg_gpu_norm_finalize(const double* partials, int32_t n_partials, double* out_dev, void* stream);
+
+/* ---- z-slab kernels (3D; pitch P = nodes-1 in {32,...,1024}) ------------
+ * Same arithmetic as the whole-level entry points above, restricted to the
+ * slab's owned planes; halo planes must have been exchanged beforehand. */
+
+/* one Jacobi step on the owned planes; u_in NULL = first step from zero
+ * (pointwise, all local planes) */
+int mpmg_gpu_slab_jacobi(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u_in, void* u_out,
+                         double omega, uint32_t policy, void* stream);
+int mpmg_gpu_slab_defect(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u, void* r,
+                         uint32_t policy, void* stream);
+/* coarse slab sc from fine slab sf (needs the fine LOWER halo of r_fine);
+ * product accumulated in fine_prec, stored in coarse_prec (scale 1) */
+int mpmg_gpu_slab_restrict(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_slab* sc, int32_t fine_prec,
+                           int32_t coarse_prec, const void* r_fine, void* r_coarse, uint32_t policy, void* stream);
+/* u_fine += P c_coarse on the fine owned planes (needs the coarse UPPER halo) */
+int mpmg_gpu_slab_prolong_correct(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_slab* sc, int32_t fine_prec,
+                                  int32_t coarse_prec, const void* c_coarse, void* u_fine, uint32_t policy,
+                                  void* stream);
+/* FP64 defect r = b - A u of the owned planes + per-CTA sums of r^2
+ * (resnorm != 0: the residual_norm form b - s, no store) */
+int mpmg_gpu_slab_defect_f64(const mpmg_stencil* A64, const mpmg_slab* s, const double* b, const double* u,
+                             double* r, double* partials, int32_t resnorm, void* stream);
+int mpmg_gpu_slab_update_rc(const mpmg_stencil* A64, const mpmg_slab* s, const void* c, int32_t c_prec, double* r,
+                            double* u, const double* alpha_dev, double* partials, uint32_t policy, void* stream);
+/* out = round(x / alpha) over the whole local slab array */
+int mpmg_gpu_slab_scale_downcast(int32_t nodes, const mpmg_slab* s, const double* x, void* out, int32_t prec,
+                                 const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream);
+/* partial sums written by slab_defect_f64 (update = 0) or slab_update_rc
+ * (update = 1, c precision c_prec) */
+int mpmg_gpu_slab_partials_len(int32_t nodes, const mpmg_slab* s, int32_t c_prec, int32_t update);
+/* *out_dev = sum of partials[0..n) in index order (no square root) */
+int mpmg_gpu_partials_sum(const double* partials, int32_t n, double* out_dev, void* stream);
 
 /* ---- generic ELLPACK path (from_levels hierarchies, public kernel API) ----
  * Device matrices are SLOT-MAJOR: val[s*rows + r], col[s*rows + r] (the
@@ -263,6 +313,11 @@ int mpmg_solver_solve_device(mpmg_solver* s, const double* b_dev, double* u_dev,
 /* One V-cycle on host buffers: b, c compact in the finest level precision,
  * passed as binary64 value-domain arrays (MgHierarchy::v_cycle). */
 int mpmg_solver_v_cycle(mpmg_solver* s, const double* b_host, double* c_host);
+
+/* One V-cycle on device buffers: b_dev, c_dev padded arrays of the finest
+ * level's precision, on `stream` (NULL: the solver's stream). Used by the
+ * multi-GPU driver for the agglomerated coarse levels. */
+int mpmg_solver_v_cycle_device(mpmg_solver* s, const void* b_dev, void* c_dev, void* stream);
 
 /* Per-level operations on host value-domain buffers (for parity tests of the
  * level kernels through the same device code the solver runs). */

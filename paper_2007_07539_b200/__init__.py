@@ -140,6 +140,17 @@ def lib():
     L.mpmg_gpu_partials_len.restype = i; L.mpmg_gpu_partials_len.argtypes = [i32, i32]
     L.mpmg_gpu_norm2_f64.restype = i; L.mpmg_gpu_norm2_f64.argtypes = [i32, i32, vp, vp, vp, vp]
     L.mpmg_gpu_norm_finalize.restype = i; L.mpmg_gpu_norm_finalize.argtypes = [vp, i32, vp, vp]
+    i64 = C.c_int64
+    L.mpmg_gpu_ell_spmv.restype = i; L.mpmg_gpu_ell_spmv.argtypes = [i64, i32, vp, vp, i32, vp, vp, u32, vp]
+    L.mpmg_gpu_axpy.restype = i; L.mpmg_gpu_axpy.argtypes = [i64, i32, d, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_vec_multiply.restype = i; L.mpmg_gpu_vec_multiply.argtypes = [i64, i32, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_ell_transfer.restype = i
+    L.mpmg_gpu_ell_transfer.argtypes = [i64, i32, vp, vp, i32, vp, i32, i32, vp, i32, vp, vp, u32, vp]
+    L.mpmg_gpu_ell_update_rc.restype = i
+    L.mpmg_gpu_ell_update_rc.argtypes = [i64, i32, vp, vp, vp, i32, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_cast.restype = i; L.mpmg_gpu_cast.argtypes = [i64, vp, i32, vp, i32, vp, d, u32, vp]
+    L.mpmg_gpu_dot_seq.restype = i; L.mpmg_gpu_dot_seq.argtypes = [i64, vp, i32, vp, i32, vp, i32, vp]
+    L.mpmg_dev_count.restype = i
     _lib = L
     return L
 

@@ -169,3 +169,104 @@ int mpmg_dev_memset0(void* p, size_t bytes) {
 int mpmg_dev_sync(void) { return rc(cudaDeviceSynchronize()); }
 
 }  // extern "C"
+
+// ---- z-slab entry points (multi-GPU slab decomposition) -------------------
+namespace {
+
+bool valid_slab(const mpmg_stencil* A, const mpmg_slab* s) {
+  return valid_stencil(A) && A->dim == 3 && s && s->nz >= 1 && s->z_lo >= 1 && s->z_lo + s->nz <= A->nodes - 1 &&
+         (A->nodes - 1) % 32 == 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t mpmg_slab_len(int32_t nodes, int32_t nz) {
+  const size_t P = (size_t)(nodes - 1);
+  return (size_t)(nz + 2) * P * P + P + 1;
+}
+
+int mpmg_gpu_slab_jacobi(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u_in, void* u_out,
+                         double omega, uint32_t policy, void* stream) {
+  if (!valid_slab(A, s) || !b || !u_out || u_in == u_out || !(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;
+  const cudaStream_t q = (cudaStream_t)stream;
+  const bool ftz = policy & MPMG_FTZ;
+  if (!u_in)
+    return rc(launch_jacobi_zero_len(mpmg_slab_len(A->nodes, s->nz), A->prec, b, u_out, round_to(omega, A->prec, ftz),
+                                     A->inv_diag, policy, q));
+  cudaError_t e = cudaSuccess;
+  bool done = false;
+  if (A->prec == MPMG_FP16) done = plane_level_op_f16(2, *A, u_in, b, u_out, omega, policy, q, &e, s);
+  else if (A->prec == MPMG_FP32) done = plane_level_op_f32(2, *A, u_in, b, u_out, omega, policy, q, &e, s);
+  else done = plane_level_op_f64(2, *A, u_in, b, u_out, omega, policy, q, &e, s);
+  return done ? rc(e) : MPMG_EUNSUPPORTED;
+}
+
+int mpmg_gpu_slab_defect(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u, void* r,
+                         uint32_t policy, void* stream) {
+  if (!valid_slab(A, s) || !b || !u || !r || u == r) return MPMG_EINVAL;
+  const cudaStream_t q = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  bool done = false;
+  if (A->prec == MPMG_FP16) done = plane_level_op_f16(1, *A, u, b, r, 1.0, policy, q, &e, s);
+  else if (A->prec == MPMG_FP32) done = plane_level_op_f32(1, *A, u, b, r, 1.0, policy, q, &e, s);
+  else done = plane_level_op_f64(1, *A, u, b, r, 1.0, policy, q, &e, s);
+  return done ? rc(e) : MPMG_EUNSUPPORTED;
+}
+
+int mpmg_gpu_slab_restrict(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_slab* sc, int32_t fine_prec,
+                           int32_t coarse_prec, const void* r_fine, void* r_coarse, uint32_t policy, void* stream) {
+  if (!sf || !sc || !r_fine || !r_coarse || !valid_prec(fine_prec) || !valid_prec(coarse_prec) ||
+      (fine_nodes - 1) % 2 || 2 * sc->z_lo < sf->z_lo || 2 * (sc->z_lo + sc->nz - 1) + 1 > sf->z_lo + sf->nz)
+    return MPMG_EINVAL;
+  return rc(launch_restrict_slab(fine_nodes, *sf, *sc, fine_prec, coarse_prec, r_fine, r_coarse, policy,
+                                 (cudaStream_t)stream));
+}
+
+int mpmg_gpu_slab_prolong_correct(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_slab* sc, int32_t fine_prec,
+                                  int32_t coarse_prec, const void* c_coarse, void* u_fine, uint32_t policy,
+                                  void* stream) {
+  if (!sf || !sc || !c_coarse || !u_fine || !valid_prec(fine_prec) || !valid_prec(coarse_prec) || (fine_nodes - 1) % 8)
+    return MPMG_EINVAL;
+  return rc(launch_prolong_slab(fine_nodes, *sf, *sc, fine_prec, coarse_prec, c_coarse, u_fine, policy,
+                                (cudaStream_t)stream));
+}
+
+int mpmg_gpu_slab_defect_f64(const mpmg_stencil* A64, const mpmg_slab* s, const double* b, const double* u,
+                             double* r, double* partials, int32_t resnorm, void* stream) {
+  if (!valid_slab(A64, s) || A64->prec != MPMG_FP64 || !b || !u || (!r && !resnorm)) return MPMG_EINVAL;
+  cudaError_t e = cudaSuccess;
+  return plane_defect64(*A64, b, u, r, partials, true, resnorm != 0, (cudaStream_t)stream, nullptr, &e, s)
+             ? rc(e)
+             : MPMG_EUNSUPPORTED;
+}
+
+int mpmg_gpu_slab_update_rc(const mpmg_stencil* A64, const mpmg_slab* s, const void* c, int32_t c_prec, double* r,
+                            double* u, const double* alpha_dev, double* partials, uint32_t policy, void* stream) {
+  if (!valid_slab(A64, s) || A64->prec != MPMG_FP64 || !c || !valid_prec(c_prec) || !r || !u || !alpha_dev)
+    return MPMG_EINVAL;
+  cudaError_t e = cudaSuccess;
+  return plane_update_rc(*A64, c, c_prec, r, u, alpha_dev, partials, policy & MPMG_FMA, (cudaStream_t)stream, &e, s)
+             ? rc(e)
+             : MPMG_EUNSUPPORTED;
+}
+
+int mpmg_gpu_slab_scale_downcast(int32_t nodes, const mpmg_slab* s, const double* x, void* out, int32_t prec,
+                                 const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream) {
+  if (!s || s->nz < 1 || nodes < 3 || !x || !out || !valid_prec(prec) || !alpha_dev) return MPMG_EINVAL;
+  return rc(launch_downcast_len(mpmg_slab_len(nodes, s->nz), x, out, prec, alpha_dev, scale_enabled, policy,
+                                (cudaStream_t)stream));
+}
+
+int mpmg_gpu_slab_partials_len(int32_t nodes, const mpmg_slab* s, int32_t c_prec, int32_t update) {
+  if (!s || s->nz < 1) return MPMG_EINVAL;
+  return plane_partials(3, nodes, c_prec, update != 0, s->nz + 1);
+}
+
+int mpmg_gpu_partials_sum(const double* partials, int32_t n, double* out_dev, void* stream) {
+  if (!partials || n < 0 || !out_dev) return MPMG_EINVAL;
+  return rc(launch_partials_sum(partials, n, out_dev, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -28,7 +28,7 @@ using namespace mpmg_dev;
 
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kCtaPoints = 4096;
 
 template <int PR> struct T_;
@@ -69,26 +69,48 @@ struct Lv {
     if constexpr (PR == P32) return f32<FTZ>(FMA ? __fmaf_rn((float)w, x, acc) : __fadd_rn(__fmul_rn((float)w, x), acc));
     else return fma(from(w), x, acc);
   }
-  // A x at padded index i (all 3^dim taps; ghosts are zero); x read via L2
-  static __device__ __forceinline__ T apply(const CoarseLevel& L, const T* x, int i, int P) {
-    const int pl = L.dim == 3 ? P * P : 0;
+  // the level's taps in the compute precision, converted once per operation
+  struct Taps {
+    T t[27];
+    float f[27];
+  };
+  static __device__ __forceinline__ Taps taps(const CoarseLevel& L) {
+    Taps k;
+    for (int t = 0; t < 27; ++t) {
+      k.t[t] = from(L.taps[t]);
+      k.f[t] = (float)L.taps[t];
+    }
+    return k;
+  }
+  // A x at padded index i (all 3^dim taps in slot order; ghosts are zero)
+  template <int DIM>
+  static __device__ __forceinline__ T apply_d(const Taps& k, const T* x, int i, int P) {
+    const int pl = DIM == 3 ? P * P : 0;
     if constexpr (PR == P16 && ACC32) {  // Fp16Accum::FP32 (kernels.cpp:151-162)
       float acc = 0.0f;
       int t = 0;
-      for (int dz = (L.dim == 3 ? -1 : 0); dz <= (L.dim == 3 ? 1 : 0); ++dz)
+#pragma unroll
+      for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
+#pragma unroll
         for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
           for (int dx = -1; dx <= 1; ++dx, ++t)
-            acc = fma32<FTZ, FMA>((float)L.taps[t], __half2float(ldcg(x + i + dz * pl + dy * P + dx)), acc);
+            acc = fma32<FTZ, FMA>(k.f[t], __half2float(ldcg(x + i + dz * pl + dy * P + dx)), acc);
       return f16s<FTZ>(__float2half_rn(acc));
     } else {
       T acc = zero();
       int t = 0;
-      for (int dz = (L.dim == 3 ? -1 : 0); dz <= (L.dim == 3 ? 1 : 0); ++dz)
+#pragma unroll
+      for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
+#pragma unroll
         for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx, ++t)
-            acc = fma(from(L.taps[t]), ldcg(x + i + dz * pl + dy * P + dx), acc);
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx, ++t) acc = fma(k.t[t], ldcg(x + i + dz * pl + dy * P + dx), acc);
       return acc;
     }
+  }
+  static __device__ __forceinline__ T apply(const Taps& k, int dim, const T* x, int i, int P) {
+    return dim == 3 ? apply_d<3>(k, x, i, P) : apply_d<2>(k, x, i, P);
   }
 };
 
@@ -133,7 +155,10 @@ template <bool FTZ, bool FMA, bool ACC32>
 struct Coarse {
   const CoarseArgs& a;
   unsigned rank, ncta;
-  __device__ Coarse(const CoarseArgs& args) : a(args), rank(cluster_rank()), ncta(cluster_size()) {}
+  CoarseLevel* lv;  // level table in shared memory: CTA 0's small levels point into shared memory
+  void* const* cgp;  // CG scratch r, p, ap, s, best
+  __device__ Coarse(const CoarseArgs& args, CoarseLevel* table, void* const* cg)
+      : a(args), rank(cluster_rank()), ncta(cluster_size()), lv(table), cgp(cg) {}
 
   template <int PR> using O = Lv<PR, FTZ, FMA, ACC32>;
 
@@ -168,8 +193,9 @@ struct Coarse {
     const T* u = static_cast<const T*>(uin);
     T* o = static_cast<T*>(uout);
     const T w = OP::from(L.omega), d = OP::from(L.inv_diag), m1 = OP::from(-1.0);
+    const auto tk = OP::taps(L);
     for_points(L, [&](int i, int P) {
-      const T t = from_zero ? OP::zero() : OP::apply(L, u, i, P);
+      const T t = from_zero ? OP::zero() : OP::apply(tk, L.dim, u, i, P);
       const T r = OP::fma(m1, t, ldcg(b + i));
       o[i] = OP::fma(w, OP::mul(d, r), from_zero ? OP::zero() : ldcg(u + i));
     });
@@ -180,8 +206,9 @@ struct Coarse {
     using OP = O<PR>;
     using T = typename OP::T;
     const T m1 = OP::from(-1.0);
+    const auto tk = OP::taps(L);
     for_points(L, [&](int i, int P) {
-      static_cast<T*>(rv)[i] = OP::fma(m1, OP::apply(L, static_cast<const T*>(uv), i, P), ldcg(static_cast<const T*>(bv) + i));
+      static_cast<T*>(rv)[i] = OP::fma(m1, OP::apply(tk, L.dim, static_cast<const T*>(uv), i, P), ldcg(static_cast<const T*>(bv) + i));
     });
   }
 
@@ -271,11 +298,11 @@ struct Coarse {
     __shared__ double sh;
     const T* b = static_cast<const T*>(bv);
     T* u = static_cast<T*>(uv);
-    T* r = static_cast<T*>(a.cg_r);
-    T* p = static_cast<T*>(a.cg_p);
-    T* ap = static_cast<T*>(a.cg_ap);
-    T* sc = static_cast<T*>(a.cg_s);
-    T* best = static_cast<T*>(a.cg_best);
+    T* r = static_cast<T*>(cgp[0]);
+    T* p = static_cast<T*>(cgp[1]);
+    T* ap = static_cast<T*>(cgp[2]);
+    T* sc = static_cast<T*>(cgp[3]);
+    T* best = static_cast<T*>(cgp[4]);
     const Pt pt = points(L);
     auto dot = [&](const T* x, const T* y) -> double {
       __syncthreads();
@@ -303,8 +330,9 @@ struct Coarse {
     double true_res = norm_b, best_res = norm_b;
     int it = 0;
     const T m1 = OP::from(-1.0);
+    const auto tk = OP::taps(L);
     while (true_res >= thr && it < max_it) {
-      each([&](int i) { ap[i] = OP::apply(L, p, i, pt.P); });
+      each([&](int i) { ap[i] = OP::apply(tk, L.dim, p, i, pt.P); });
       const double pAp = dot(p, ap);
       if (!(pAp > 0.0) || !isfinite(pAp)) break;
       const double alpha = rz / pAp;
@@ -315,7 +343,7 @@ struct Coarse {
       });
       const double rz_new = dot(r, r);
       ++it;
-      each([&](int i) { sc[i] = OP::apply(L, u, i, pt.P); });
+      each([&](int i) { sc[i] = OP::apply(tk, L.dim, u, i, pt.P); });
       each([&](int i) { sc[i] = OP::fma(m1, ldcg(sc + i), ldcg(b + i)); });
       true_res = sqrt(dot(sc, sc));
       if (true_res < best_res) {
@@ -356,14 +384,29 @@ struct Coarse {
   // whole cluster and followed by a cluster barrier. The one extra cluster
   // barrier before prolongating a small level's correction into a big level
   // publishes CTA 0's small-level results.
+  int entry = -1;  // highest level worked by CTA 0 alone (its b arrives in global memory)
+
+  // global b of the entry level -> CTA 0's shared copy
+  __device__ void stage_in(int l) {
+    if (rank == 0) copy_level(lv[l], a.lv[l].b, lv[l].b);
+    __syncthreads();
+  }
+  __device__ void stage_out(int l, const void* src) {
+    if (rank == 0) copy_level(lv[l], src, a.lv[l].u);
+    __syncthreads();
+  }
+
   __device__ void run() {
     __shared__ double scales[kMaxCoarseLevels];
     void* cur[kMaxCoarseLevels];
     const int top = a.nlev - 1;
+    for (int l = top; l >= 0; --l)
+      if (small(lv[l])) { entry = l; break; }
     // down-sweep (cycle_at before the recursive call)
     for (int l = top; l >= 1; --l) {
-      const CoarseLevel& L = a.lv[l];
-      const CoarseLevel& C = a.lv[l - 1];
+      const CoarseLevel& L = lv[l];
+      const CoarseLevel& C = lv[l - 1];
+      if (small(L) && l == entry) stage_in(l);
       void* u = smooth(L, nullptr, a.pre);
       if (u == nullptr) {  // pre_steps == 0: u = 0
         if (in_team(L)) for_points(L, [&](int i, int) {
@@ -401,8 +444,18 @@ struct Coarse {
       }
     }
     // base solve on CTA 0
+    if (top == 0 && entry == 0) {
+      // single-level call (OP_COARSE_SOLVE): result to global
+      stage_in(0);
+      if (rank == 0) by_prec(lv[0].prec, [&](auto pc) { cg<decltype(pc)::value>(lv[0], lv[0].b, lv[0].u); });
+      __syncthreads();
+      if (rank == 0) copy_level(lv[0], lv[0].u, a.lv[0].u);
+      __syncthreads();
+      return;
+    }
     {
-      const CoarseLevel& B = a.lv[0];
+      const CoarseLevel& B = lv[0];
+      if (entry == 0) stage_in(0);
       if (rank == 0) by_prec(B.prec, [&](auto pc) { cg<decltype(pc)::value>(B, B.b, B.u); });
       __syncthreads();
       if (!small(B)) cluster_sync();
@@ -410,9 +463,13 @@ struct Coarse {
     }
     // up-sweep
     for (int l = 1; l <= top; ++l) {
-      const CoarseLevel& L = a.lv[l];
-      const CoarseLevel& C = a.lv[l - 1];
-      if (!small(L) && small(C)) cluster_sync();
+      const CoarseLevel& L = lv[l];
+      const CoarseLevel& C = lv[l - 1];
+      if (!small(L) && small(C)) {
+        stage_out(l - 1, cur[l - 1]);  // CTA 0's shared-memory correction -> global
+        cur[l - 1] = a.lv[l - 1].u;
+        cluster_sync();
+      }
       if (in_team(L)) {
         by_prec(L.prec, [&](auto fp) {
           by_prec(C.prec, [&](auto cp) {
@@ -422,19 +479,67 @@ struct Coarse {
       }
       sync(L);
       void* u = smooth(L, cur[l], a.post);
-      if (l == top && u != L.u) {  // the caller reads the top correction from L.u
-        if (in_team(L)) copy_level(L, u, L.u);
+      if (l == top && u != a.lv[top].u) {  // the caller reads the top correction from global L.u
+        if (in_team(L)) copy_level(L, u, a.lv[top].u);
         sync(L);
-        u = L.u;
+        u = a.lv[top].u;
       }
       cur[l] = u;
     }
   }
 };
 
+__host__ __device__ inline long long padded_of(const CoarseLevel& L) {
+  const long long P = L.nodes - 1;
+  return L.dim == 3 ? P * P * P + P * P + P + 1 : P * P + P + 1;
+}
+__host__ __device__ inline int bytes_of(int prec) { return prec == MPMG_FP16 ? 2 : (prec == MPMG_FP32 ? 4 : 8); }
+__host__ __device__ inline bool small_level(const CoarseLevel& L) {
+  const long long m = L.nodes - 2;
+  return (L.dim == 3 ? m * m * m : m * m) <= kCtaPoints;
+}
+
+// shared bytes for CTA 0's small levels (u, u2, b, r each, 16-byte aligned)
+// plus the CG scratch of level 0
+__host__ __device__ inline size_t coarse_smem(const CoarseArgs& a) {
+  size_t n = 0;
+  for (int l = 0; l < a.nlev; ++l)
+    if (small_level(a.lv[l])) n += 4 * ((padded_of(a.lv[l]) * bytes_of(a.lv[l].prec) + 15) / 16 * 16);
+  if (small_level(a.lv[0])) n += 5 * ((padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16);
+  return n;
+}
+
 template <bool FTZ, bool FMA, bool ACC32>
-__global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a) {
-  Coarse<FTZ, FMA, ACC32> c(a);
+__global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a, int use_smem) {
+  __shared__ CoarseLevel table[kMaxCoarseLevels];
+  __shared__ void* cg[5];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  if (threadIdx.x == 0) {
+    for (int l = 0; l < a.nlev; ++l) table[l] = a.lv[l];
+    cg[0] = a.cg_r; cg[1] = a.cg_p; cg[2] = a.cg_ap; cg[3] = a.cg_s; cg[4] = a.cg_best;
+    if (use_smem && cluster_rank() == 0) {
+      unsigned char* p = dyn;
+      for (int l = 0; l < a.nlev; ++l) {
+        if (!small_level(a.lv[l])) continue;
+        const size_t b = (padded_of(a.lv[l]) * bytes_of(a.lv[l].prec) + 15) / 16 * 16;
+        table[l].u = p; p += b;
+        table[l].u2 = p; p += b;
+        table[l].b = p; p += b;
+        table[l].r = p; p += b;
+      }
+      if (small_level(a.lv[0])) {
+        const size_t b = (padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16;
+        for (int k = 0; k < 5; ++k) { cg[k] = p; p += b; }
+      }
+    }
+  }
+  __syncthreads();
+  if (use_smem && cluster_rank() == 0) {  // ghosts must read as zero
+    const size_t n = coarse_smem(a) / 16;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  Coarse<FTZ, FMA, ACC32> c(a, table, cg);
   c.run();
 }
 
@@ -464,7 +569,11 @@ cudaError_t launch_t(const CoarseArgs& a, cudaStream_t s) {
     cudaGetLastError();
   }
   const int csize = n > kCtaPoints ? max_cluster : 1;
+  const size_t smem = coarse_smem(a);
+  const int use_smem = smem <= 200 * 1024 ? 1 : 0;
+  if (use_smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
+  cfg.dynamicSmemBytes = use_smem ? smem : 0;
   cfg.gridDim = dim3(csize);
   cfg.blockDim = dim3(kThreads);
   cfg.stream = s;
@@ -473,7 +582,7 @@ cudaError_t launch_t(const CoarseArgs& a, cudaStream_t s) {
   at[0].val.clusterDim.x = csize; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  return cudaLaunchKernelEx(&cfg, kern, a, use_smem);
 }
 
 }  // namespace

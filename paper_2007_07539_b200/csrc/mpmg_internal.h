@@ -42,17 +42,20 @@ cudaError_t launch_update_rc(const mpmg_stencil& A64, const void* c, int c_prec,
 int stencil_partials(int dim, int nodes, int lp, bool update);
 // TMA-staged plane kernels (mpmg_plane_*.cu): return false when the shape
 // or policy is not covered (the caller then uses the streaming kernels)
+// (slab: a z-slab of the level, include/mpmg_gpu.h; nullptr = the whole level)
 bool plane_level_op_f16(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
-                        uint32_t policy, cudaStream_t s, cudaError_t* err);
+                        uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
 bool plane_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
-                        uint32_t policy, cudaStream_t s, cudaError_t* err);
+                        uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
 bool plane_level_op_f64(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
-                        uint32_t policy, cudaStream_t s, cudaError_t* err);
+                        uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
 bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
-                    bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err);
+                    bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err,
+                    const mpmg_slab* slab = nullptr);
 bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
-                     const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err);
-int plane_partials(int dim, int nodes, int lp, bool update);
+                     const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err,
+                     const mpmg_slab* slab = nullptr);
+int plane_partials(int dim, int nodes, int lp, bool update, int pz = 0);
 // true when the streaming stencil kernels support this level shape
 bool stencil_supported(int dim, int nodes, int prec);
 
@@ -65,10 +68,19 @@ cudaError_t launch_restrict(int dim, int fine_nodes, int fine_prec, int coarse_p
                             void* r_coarse, const double* scale_dev, uint32_t policy, cudaStream_t s);
 cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_prec, const void* c_coarse,
                            void* u_fine, const double* scale_dev, uint32_t policy, cudaStream_t s);
+cudaError_t launch_jacobi_zero_len(size_t len, int prec, const void* b, void* u, double omega_r, double invdiag_r,
+                                   uint32_t policy, cudaStream_t s);
+cudaError_t launch_downcast_len(size_t len, const double* x, void* out, int prec, const double* alpha_dev,
+                                int scale_enabled, uint32_t policy, cudaStream_t s);
+cudaError_t launch_restrict_slab(int fine_nodes, const mpmg_slab& sf, const mpmg_slab& sc, int fine_prec,
+                                 int coarse_prec, const void* r_fine, void* r_coarse, uint32_t policy, cudaStream_t s);
+cudaError_t launch_prolong_slab(int fine_nodes, const mpmg_slab& sf, const mpmg_slab& sc, int fine_prec,
+                                int coarse_prec, const void* c_coarse, void* u_fine, uint32_t policy, cudaStream_t s);
 cudaError_t launch_downcast(int dim, int nodes, const double* x, void* out, int prec, const double* alpha_dev,
                             int scale_enabled, uint32_t policy, cudaStream_t s);
 cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* out, cudaStream_t s);
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
+cudaError_t launch_partials_sum(const double* partials, int n, double* out, cudaStream_t s);
 int norm2_partials(size_t len);
 cudaError_t launch_fill_random01(double* padded_u, int dim, int nodes, uint64_t seed, cudaStream_t s);
 

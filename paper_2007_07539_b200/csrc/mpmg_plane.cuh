@@ -39,6 +39,10 @@ enum { POP_SPMV = 0, POP_DEFECT = 1, POP_JACOBI = 2, POP_DEFECT64 = 3, POP_RESNO
 struct PlaneArgs {
   int P;             // pitch
   int zc;            // output planes per CTA
+  int pz;            // index of the last local plane: outputs are planes 1 .. pz-1
+                     // (a whole level: pz = P; a z-slab of nz owned planes: nz + 1)
+  int load_lo;       // plane 0 holds data (a neighbour's halo) -- else a zero ghost, skipped
+  int load_hi;       // plane pz holds data
   int ty;            // output rows per CTA (WY*RY)
   long long plane;   // P*P
   __half2 t16[27];
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
   const int tr = wy * RY;  // tile row of this thread's first output row (minus 1)
   const int y0 = 1 + (int)blockIdx.x * TY;
   const int z0 = 1 + (int)blockIdx.y * a.zc;
-  const int z1 = min(z0 + a.zc, P);  // outputs [z0, z1)
+  const int z1 = min(z0 + a.zc, a.pz);  // outputs [z0, z1)
   const int NQ = z1 - z0 + 2;        // planes z0-1 .. z1
   const long long plane = (long long)P * P;
   const int xrows = min(y0 + TY, P) - y0 + 2;  // operand rows y0-1 .. min(y0+TY, P)
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
 
   auto issue = [&](int k) {  // one elected thread: plane k into stage k % NS
     const int q = z0 - 1 + k;
-    if (q < 1 || q > P - 1) return;  // ghost planes are never loaded
+    if ((q == 0 && !a.load_lo) || (q == a.pz && !a.load_hi)) return;  // zero ghost planes are never loaded
     unsigned char* st = stages + (k % NS) * K::kStage;
     uint64_t* bar = full + (k % NS);
     const uint32_t xb = (uint32_t)(xrows * K::kXRow);
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
     const int s = k % NS;
     const unsigned char* st = stages + s * K::kStage;
     prefetch_b(q);
-    if (q >= 1 && q <= P - 1) {
+    if ((q > 0 || a.load_lo) && (q < a.pz || a.load_hi)) {
       mbar_wait(full + s, (phase >> s) & 1u);
       phase ^= 1u << s;
       // acc0: output q-1 (ours iff k >= 2), acc1: q (1 <= k <= NQ-2), acc2: q+1 (k <= NQ-3)

@@ -29,9 +29,13 @@ inline __half2 h2_of(double v) {
   return __halves2half2(h, h);
 }
 
-inline PlaneArgs plane_args(const mpmg_stencil& A) {
+// slab: nz owned planes with halo flags, or nullptr for the whole level
+inline PlaneArgs plane_args(const mpmg_stencil& A, const mpmg_slab* slab = nullptr) {
   PlaneArgs a{};
   a.P = pitch(A.nodes);
+  a.pz = slab ? slab->nz + 1 : a.P;
+  a.load_lo = slab ? slab->halo_lo : 0;
+  a.load_hi = slab ? slab->halo_hi : 0;
   a.plane = (long long)a.P * a.P;
   for (int i = 0; i < 27; ++i) {
     const double t = i < A.ntaps ? A.taps[i] : 0.0;
@@ -56,7 +60,7 @@ struct PlaneLaunch {
   static constexpr auto kernel = k_plane<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS>;
 
   // grid: y-tiles x z-chunks, z-chunks sized so the grid is about one wave
-  static dim3 grid(int* zc) {
+  static dim3 grid(int* zc, int pz = P) {
     static int per_sm = -1;
     if (per_sm < 0) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem);
@@ -68,28 +72,28 @@ struct PlaneLaunch {
     const int cap = per_sm * plane_num_sms();
     int chunks = cap / ytiles;
     if (chunks < 1) chunks = 1;
-    if (chunks > P - 1) chunks = P - 1;
-    int z = (P - 1 + chunks - 1) / chunks;
+    if (chunks > pz - 1) chunks = pz - 1;
+    int z = (pz - 1 + chunks - 1) / chunks;
     // small grids are latency-bound: as many CTAs as possible; large grids
     // keep >= 2 planes per chunk so the z-halo re-reads stay small
     const int zmin = P >= 256 ? 2 : 1;
     if (z < zmin) z = zmin;
     *zc = z;
-    return dim3(ytiles, (P - 1 + z - 1) / z, 1);
+    return dim3(ytiles, (pz - 1 + z - 1) / z, 1);
   }
 
   static cudaError_t run(PlaneArgs a, cudaStream_t s) {
     int zc = 0;
-    const dim3 g = grid(&zc);
+    const dim3 g = grid(&zc, a.pz);
     a.zc = zc;
     a.ty = K::TY;
     kernel<<<g, K::kThreads, K::kSmem, s>>>(a);
     return cudaGetLastError();
   }
 
-  static int partials() {
+  static int partials(int pz = P) {
     int zc = 0;
-    const dim3 g = grid(&zc);
+    const dim3 g = grid(&zc, pz);
     return (int)(g.x * g.y);
   }
 };
@@ -121,12 +125,12 @@ inline bool faces_zero16(const mpmg_stencil& A) {
 // level op (DEFECT / JACOBI) through the plane kernels; false if not covered
 template <int LP>
 bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
-                    uint32_t policy, cudaStream_t s, cudaError_t* err) {
+                    uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr) {
   if (A.dim != 3 || (op != 1 && op != 2)) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
   if (LP == P16 && !faces_zero16(A)) return false;
   if (!aligned16(x) || !aligned16(b) || !aligned16(out)) return false;
-  PlaneArgs a = plane_args(A);
+  PlaneArgs a = plane_args(A, slab);
   a.x = x; a.b = b; a.out = out;
   const bool ftz = policy & MPMG_FTZ;
   const double w = round_to(omega, LP, ftz);

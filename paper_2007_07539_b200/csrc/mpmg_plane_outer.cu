@@ -25,9 +25,9 @@ bool plane_outer_supported(int dim, int nodes) {
 }
 
 bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
-                    bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err) {
+                    bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err, const mpmg_slab* slab) {
   if (!plane_outer_supported(A64.dim, A64.nodes) || !aligned16(b) || !aligned16(u) || !aligned16(r)) return false;
-  PlaneArgs a = plane_args(A64);
+  PlaneArgs a = plane_args(A64, slab);
   a.x = u; a.b = b; a.out = r; a.partials = partials; a.gate = gate;
   return with_pitch(a.P, [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
@@ -38,9 +38,10 @@ bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, d
 }
 
 bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double* r, double* u,
-                     const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err) {
+                     const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err,
+                     const mpmg_slab* slab) {
   if (!plane_outer_supported(A64.dim, A64.nodes) || !aligned16(c) || !aligned16(r) || !aligned16(u)) return false;
-  PlaneArgs a = plane_args(A64);
+  PlaneArgs a = plane_args(A64, slab);
   a.x = c; a.r64 = r; a.u64 = u; a.alpha = alpha_dev; a.partials = partials;
   return with_pitch(a.P, [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
@@ -61,16 +62,17 @@ bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double*
 // FP64 defect / residual norm (lp == FP64); -1 when not covered
 // (FMA on/off and DEFECT64/RESNORM instantiations share the shared-memory
 // footprint, hence the occupancy and the grid)
-int plane_partials(int dim, int nodes, int lp, bool update) {
+int plane_partials(int dim, int nodes, int lp, bool update, int pz) {
   if (!plane_outer_supported(dim, nodes)) return -1;
   int n = -1;
+  if (pz <= 0) pz = pitch(nodes);
   with_pitch(pitch(nodes), [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
-    if (!update) { n = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::partials(); return; }
+    if (!update) { n = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::partials(pz); return; }
     switch (lp) {
-      case MPMG_FP16: n = PlaneLaunch<P16, P64, P64, POP_UPDATE, false, true, PP>::partials(); break;
-      case MPMG_FP32: n = PlaneLaunch<P32, P64, P64, POP_UPDATE, false, true, PP>::partials(); break;
-      default: n = PlaneLaunch<P64, P64, P64, POP_UPDATE, false, true, PP>::partials(); break;
+      case MPMG_FP16: n = PlaneLaunch<P16, P64, P64, POP_UPDATE, false, true, PP>::partials(pz); break;
+      case MPMG_FP32: n = PlaneLaunch<P32, P64, P64, POP_UPDATE, false, true, PP>::partials(pz); break;
+      default: n = PlaneLaunch<P64, P64, P64, POP_UPDATE, false, true, PP>::partials(pz); break;
     }
   });
   return n;

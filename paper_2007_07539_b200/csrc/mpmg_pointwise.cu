@@ -112,7 +112,8 @@ template <> __device__ __forceinline__ double store_round<P64, false>(double v) 
 // neighbours of (2cx,2cy,2cz) in lexicographic order with weights
 // prod_d (d == 0 ? 1 : 1/2) (mesh_fem.cpp:266-293).
 template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
-__global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_, int Pc, const double* scale_dev) {
+__global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_, int Pc, const double* scale_dev,
+                           int zoff = 0) {
   using X = Xfer<FP, FTZ, FMA>;
   using TF = typename X::T;
   const TF* rf = static_cast<const TF*>(rf_);
@@ -123,7 +124,9 @@ __global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_,
   const int Pf = 2 * Pc;
   const long long pf = DIM == 3 ? (long long)Pf * Pf : (long long)Pf;
   TF acc = X::zero();
-  const long long cf = (DIM == 3 ? (long long)(2 * cz) * pf : 0) + (long long)(2 * cy) * Pf + 2 * cx;
+  // fine plane of coarse (local) plane cz: 2 cz + zoff (zoff = 0 for a whole
+  // level; for z-slabs the local plane numbering of the two levels differs)
+  const long long cf = (DIM == 3 ? (long long)(2 * cz + zoff) * pf : 0) + (long long)(2 * cy) * Pf + 2 * cx;
 #pragma unroll
   for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
 #pragma unroll
@@ -235,18 +238,30 @@ template <> struct V8<P64> {
 };
 
 // downcast of n8 groups of 8 values (len - 8*n8 tail done by block 0)
+// x / s correctly rounded without a per-element division (the scale is one
+// scalar for the whole vector): y = RN(1/s), q = RN(x y), e = x - s q (exact
+// via fma), q' = RN(q + e y). With y the correctly rounded reciprocal this is
+// the correctly rounded quotient (Markstein's theorem), bitwise equal to
+// __ddiv_rn -- checked exhaustively-by-sample in tests/test_gpu_parity.py.
+__device__ __forceinline__ double div_by(double x, double s, double y) {
+  const double q = __dmul_rn(x, y);
+  const double e = __fma_rn(-s, q, x);
+  return __fma_rn(e, y, q);
+}
+
 template <int PREC, bool FTZ>
 __global__ void k_downcast8(const double* __restrict__ x, void* __restrict__ out, long long len,
                             const double* alpha, int scale_enabled) {
   const double a = *alpha;
   const double s = (scale_enabled && a > 0.0) ? a : 1.0;
+  const double y = __drcp_rn(s);
   const long long n8 = len / 8;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n8; g += (long long)gridDim.x * blockDim.x) {
     V8<P64> in;
     in.load(x, 8 * g);
     V8<PREC> o;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o.set(e, store_round<PREC, FTZ>(__ddiv_rn(in.get(e), s)));
+    for (int e = 0; e < 8; ++e) o.set(e, store_round<PREC, FTZ>(s == 1.0 ? in.get(e) : div_by(in.get(e), s, y)));
     o.store(out, 8 * g);
   }
   if (blockIdx.x == 0 && threadIdx.x < len - 8 * n8) {
@@ -288,7 +303,8 @@ __global__ void k_jacobi_zero8(const void* __restrict__ bv, void* __restrict__ u
 // prolongation + correction, 8 consecutive fine x per thread (Pf % 8 == 0);
 // same parent order and rounding as k_prolong
 template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
-__global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_, int Pf, const double* scale_dev) {
+__global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_, int Pf, const double* scale_dev,
+                           int zf_lo = 1, int zc_lo = 1) {
   using X = Xfer<CPc, FTZ, FMA>;
   using TC = typename X::T;
   const TC* cc = static_cast<const TC*>(cc_);
@@ -297,12 +313,13 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
   if (g >= groups * (Pf - 1)) return;
   const int fy = g / groups + 1;
   const int x0 = (g % groups) * 8;
-  const int fz = DIM == 3 ? (int)blockIdx.y + 1 : 0;
+  const int fz = DIM == 3 ? (int)blockIdx.y + 1 : 0;  // local plane
+  const int gz = fz + zf_lo - 1;                       // global plane (parity, parents)
   const int Pc = Pf / 2;
-  const int ny = (fy & 1) ? 2 : 1, nz = DIM == 3 ? ((fz & 1) ? 2 : 1) : 1;
+  const int ny = (fy & 1) ? 2 : 1, nz = DIM == 3 ? ((gz & 1) ? 2 : 1) : 1;
   const int py[2] = {fy >> 1, (fy + 1) >> 1};
-  const int pz[2] = {fz >> 1, (fz + 1) >> 1};
-  const double wy = (fy & 1) ? 0.5 : 1.0, wz = DIM == 3 ? ((fz & 1) ? 0.5 : 1.0) : 1.0;
+  const int pz[2] = {(gz >> 1) - zc_lo + 1, ((gz + 1) >> 1) - zc_lo + 1};
+  const double wy = (fy & 1) ? 0.5 : 1.0, wz = DIM == 3 ? ((gz & 1) ? 0.5 : 1.0) : 1.0;
   // coarse values x0/2 .. x0/2+4 of each parent row
   TC c[2][2][5];
 #pragma unroll
@@ -359,7 +376,7 @@ __global__ void k_sumsq(const double* __restrict__ x, long long len, double* par
   }
 }
 
-__global__ void k_finalize(const double* __restrict__ partials, int n, double* out) {
+__global__ void k_finalize(const double* __restrict__ partials, int n, double* out, int take_sqrt = 1) {
   __shared__ double red[kThreads];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n; i += kThreads) acc += partials[i];
@@ -369,7 +386,7 @@ __global__ void k_finalize(const double* __restrict__ partials, int n, double* o
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = sqrt(red[0]);
+  if (threadIdx.x == 0) *out = take_sqrt ? sqrt(red[0]) : red[0];
 }
 
 // SplitMix64 U[0,1) initial guess (ir_solver.cpp:80-84, rng.hpp:13-25): the
@@ -423,7 +440,11 @@ cudaError_t launch_pack(int dim, int nodes, int prec, const void* compact, void*
 
 cudaError_t launch_jacobi_zero(int dim, int nodes, int prec, const void* b, void* u, double omega_r,
                                double invdiag_r, uint32_t policy, cudaStream_t s) {
-  const size_t len = mpmg_padded_len(dim, nodes);
+  return launch_jacobi_zero_len(mpmg_padded_len(dim, nodes), prec, b, u, omega_r, invdiag_r, policy, s);
+}
+
+cudaError_t launch_jacobi_zero_len(size_t len, int prec, const void* b, void* u, double omega_r, double invdiag_r,
+                                   uint32_t policy, cudaStream_t s) {
   const bool vec = aligned64(b) && aligned64(u);
   return with_prec(prec, [&](auto pc) -> cudaError_t {
     return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
@@ -480,9 +501,52 @@ cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_pr
   });
 }
 
+// z-slab transfers (3D): coarse local planes 1..nzc from fine slab planes
+// (fine local plane 0 = the lower halo); prolongation of fine local planes
+// 1..nzf from coarse local planes (coarse local nzc+1 = the upper halo)
+cudaError_t launch_restrict_slab(int fine_nodes, const mpmg_slab& sf, const mpmg_slab& sc, int fine_prec,
+                                 int coarse_prec, const void* r_fine, void* r_coarse, uint32_t policy,
+                                 cudaStream_t s) {
+  const int Pc = pitch(fine_nodes) / 2;
+  if (Pc < 2 || sc.nz < 1) return cudaSuccess;
+  const dim3 block(32, 8);
+  const dim3 grid((Pc - 1 + 31) / 32, (Pc - 1 + 7) / 8, sc.nz);
+  const int zoff = 2 * sc.z_lo - sf.z_lo - 1;
+  return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
+    return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
+      return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+        k_restrict<3, decltype(fp)::value, decltype(cp)::value, decltype(ft)::value, decltype(fm)::value>
+            <<<grid, block, 0, s>>>(r_fine, r_coarse, Pc, nullptr, zoff);
+        return cudaGetLastError();
+      });
+    });
+  });
+}
+
+cudaError_t launch_prolong_slab(int fine_nodes, const mpmg_slab& sf, const mpmg_slab& sc, int fine_prec,
+                                int coarse_prec, const void* c_coarse, void* u_fine, uint32_t policy,
+                                cudaStream_t s) {
+  const int Pf = pitch(fine_nodes);
+  if (Pf % 8 || !aligned64(u_fine) || sf.nz < 1) return cudaErrorInvalidValue;
+  const dim3 grid8v((unsigned)(((Pf / 8) * (Pf - 1) + kThreads - 1) / kThreads), sf.nz);
+  return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
+    return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
+      return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+        k_prolong8<3, decltype(fp)::value, decltype(cp)::value, decltype(ft)::value, decltype(fm)::value>
+            <<<grid8v, kThreads, 0, s>>>(c_coarse, u_fine, Pf, nullptr, sf.z_lo, sc.z_lo);
+        return cudaGetLastError();
+      });
+    });
+  });
+}
+
 cudaError_t launch_downcast(int dim, int nodes, const double* x, void* out, int prec, const double* alpha_dev,
                             int scale_enabled, uint32_t policy, cudaStream_t s) {
-  const size_t len = mpmg_padded_len(dim, nodes);
+  return launch_downcast_len(mpmg_padded_len(dim, nodes), x, out, prec, alpha_dev, scale_enabled, policy, s);
+}
+
+cudaError_t launch_downcast_len(size_t len, const double* x, void* out, int prec, const double* alpha_dev,
+                                int scale_enabled, uint32_t policy, cudaStream_t s) {
   const unsigned blocks = std::min<unsigned>(blocks_for(len, 4), 148u * 16u);
   if (aligned64(x) && aligned64(out))
     return with_prec(prec, [&](auto pc) -> cudaError_t {
@@ -509,6 +573,11 @@ cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* 
   const int nb = norm2_partials(len);
   k_sumsq<<<nb, kThreads, 0, s>>>(x, (long long)len, partials);
   k_finalize<<<1, kThreads, 0, s>>>(partials, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_partials_sum(const double* partials, int n, double* out, cudaStream_t s) {
+  k_finalize<<<1, kThreads, 0, s>>>(partials, n, out, 0);
   return cudaGetLastError();
 }
 

@@ -668,6 +668,24 @@ int mpmg_solver_v_cycle(mpmg_solver* S, const double* b_host, double* c_host) {
   return finish(e);
 }
 
+int mpmg_solver_v_cycle_device(mpmg_solver* S, const void* b_dev, void* c_dev, void* stream) {
+  if (!S || !b_dev || !c_dev) return MPMG_EINVAL;
+  Level& F = S->lv.back();
+  const cudaStream_t q = stream ? (cudaStream_t)stream : S->s;
+  void* saved = F.b;
+  F.b = S->rlow;
+  if (S->nc == (int)S->lv.size()) S->cargs.lv[S->nc - 1].b = F.b;
+  S->gvalid = false;
+  const size_t bytes = F.len * F.bytes;
+  cudaError_t e = cudaMemcpyAsync(F.b, b_dev, bytes, cudaMemcpyDeviceToDevice, q);
+  void* c = nullptr;
+  if (e == cudaSuccess) e = S->v_cycle(q, &c);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c_dev, c, bytes, cudaMemcpyDeviceToDevice, q);
+  F.b = saved;
+  if (S->nc == (int)S->lv.size()) S->cargs.lv[S->nc - 1].b = saved;
+  return finish(e);
+}
+
 // Per-level ops on host value-domain buffers (parity tests):
 //  SPMV     out = A_l in0
 //  JACOBI   out = `steps` Jacobi steps on A_l u = in1 from u = in0 (in0 NULL: from zero)
