@@ -195,6 +195,7 @@ def run_b200(a):
             rep = h.ir_solve_ptr(bd, ud, cfg, device=True)  # CUDA events on the solver stream
             times.append(rep.device_seconds)
             its.append(rep.iterations)
+            graph_used = rep.used_graph
             assert rep.converged, f"{variant} did not converge"
         torch.cuda.synchronize()
         if ws > 1:
@@ -205,7 +206,7 @@ def run_b200(a):
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             t = float(tt.item())
         results[tag] = dict(variant=variant, seconds=t, iterations=int(its[-1]), min_s=float(np.min(times)),
-                            final_residual=rep.final_residual)
+                            final_residual=rep.final_residual, graph=bool(graph_used))
         launches_per_solve[tag] = solve_launches(h, its[-1], a)
         if tag == "mixed":
             # e2e through the public C ABI with pinned HOST buffers: H2D of b,
@@ -252,6 +253,7 @@ def run_b200(a):
                    "l2": "flushed (512 MiB write) before every timed solve; finest FP64 vectors 3x133 MB > L2",
                    "parallelism": "replicas only (one independent solve per GPU)" if ws > 1 else "1 GPU"},
         "iterations": mix["iterations"],
+        "cuda_graph": mix["graph"],
         "final_residual": mix["final_residual"],
         "tolerance": tol,
     }
@@ -463,10 +465,81 @@ def run_reference(a):
     print(json.dumps(out), flush=True)
 
 
+def run_dist(a):
+    """N > 1: the z-slab decomposed solve (paper_2007_07539_b200.dist) of the
+    same workload over NCCL, one rank per GPU; time = max over ranks of the
+    CUDA-event time of one solve (strong scaling: the problem is fixed)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_07539_b200 as mg
+    from paper_2007_07539_b200.dist import Comm, CudaOps, SlabPlan, SlabSolver, slab_of_compact
+
+    ws, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dim, n = a.dim, a.nodes
+    L = a.levels or max_depth(n)
+    ftz = bool(a.ftz)
+    b = mg.problem_rhs(dim, n)
+    tol = a.rel_tol * float(np.sqrt(np.dot(b, b)))
+    plan = SlabPlan(n, L, ws)
+    ops = CudaOps(plan, a.variant, ftz, pre=a.pre, post=a.post)
+    comm = Comm(dist, rank, ws, device_tensors=True)
+    S = SlabSolver(plan, ops, comm)
+    bs = slab_of_compact(b, plan, rank, torch, "cuda")
+    stream = torch.cuda.current_stream()
+    times, its, final = [], 0, 0.0
+    for k in range(a.warmup + a.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        u, its, hist, conv, final = S.solve(bs, tol)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if k >= a.warmup:
+            times.append(e0.elapsed_time(e1) * 1e-3)
+    t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # end to end: this rank's host rhs slab in, host solution slab out
+    dist.barrier()
+    t0 = time.perf_counter()
+    bh = slab_of_compact(b, plan, rank, torch, "cpu").pin_memory()
+    bd = bh.to("cuda", non_blocking=True)
+    u, its2, _, _, _ = S.solve(bd, tol)
+    uh = u.cpu()
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        N = mg.unknowns(dim, n)
+        out = {"metric": METRIC, "value": float(t.item()), "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+               "warmup": a.warmup, "ms_per_step": float(t.item()) * 1e3, "higher_is_better": False,
+               "scaling": "strong", "vs_baseline": None, "dtype": "fp16" if a.variant == "h_mg" else "mixed",
+               "data": "synthetic: the reference's manufactured Poisson problem, u0 = 0",
+               "config": {"workload": f"{dim}D Poisson {n}^{dim} ({N} unknowns), L={L}, V({a.pre},{a.post}), "
+                                      f"{a.variant.upper()} IR to {a.rel_tol:g}*||b||, z-slabs over {ws} GPUs",
+                          "variant": a.variant, "policy": {"flush_subnormals_to_zero": ftz, "fused_multiply_add": True},
+                          "parallelism": f"z-slab decomposition x{ws} (NCCL halo exchange), coarse levels <= "
+                                         f"{plan.P[plan.agg]}^3 agglomerated on rank 0",
+                          "l2": "no flush (strong-scaling run)"},
+               "iterations": its, "final_residual": final, "tolerance": tol, "converged": bool(final < tol),
+               "e2e": {"value": float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(bh.numel() * 8 * ws),
+                       "d2h_bytes_per_step": int(uh.numel() * 8 * ws), "path": "dist.SlabSolver (host slabs)"},
+               "gpu_launches": None}
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     a = parse()
+    ws = dist_info()[0]
     if a.impl == "reference":
         run_reference(a)
+    elif ws > 1:
+        run_dist(a)
     else:
         run_b200(a)
 

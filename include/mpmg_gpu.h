@@ -277,6 +277,8 @@ typedef struct mpmg_solve_report {   /* SolveReport (ir_solver.hpp:26-44) */
   double final_residual;
   double device_seconds;             /* CUDA-event time of the solve */
   double wall_seconds;
+  int32_t used_graph;                /* 1: the solve ran as one CUDA graph */
+  int32_t graph_error;               /* cudaError_t of a failed graph build (0: none) */
 } mpmg_solve_report;
 
 void mpmg_solver_default_config(mpmg_solver_config* cfg);
@@ -313,6 +315,11 @@ int mpmg_solver_solve_device(mpmg_solver* s, const double* b_dev, double* u_dev,
 /* One V-cycle on host buffers: b, c compact in the finest level precision,
  * passed as binary64 value-domain arrays (MgHierarchy::v_cycle). */
 int mpmg_solver_v_cycle(mpmg_solver* s, const double* b_host, double* c_host);
+
+/* Diagnostics: per-phase clock64 stamps of the last coarse-kernel run
+ * (solver created with MPMG_COARSE_DEBUG=1 in the environment). out[0] =
+ * count, out[1..] = (phase*100 + level) * 1e12 + cycles. */
+int mpmg_solver_coarse_debug(mpmg_solver* s, long long* out, int32_t cap);
 
 /* One V-cycle on device buffers: b_dev, c_dev padded arrays of the finest
  * level's precision, on `stream` (NULL: the solver's stream). Used by the

@@ -81,7 +81,8 @@ class SolveParams(C.Structure):
 
 class SolveReportC(C.Structure):
     _fields_ = [("converged", C.c_int32), ("iterations", C.c_int32), ("final_residual", C.c_double),
-                ("device_seconds", C.c_double), ("wall_seconds", C.c_double)]
+                ("device_seconds", C.c_double), ("wall_seconds", C.c_double), ("used_graph", C.c_int32),
+                ("graph_error", C.c_int32)]
 
 
 _lib = None
@@ -200,6 +201,8 @@ class SolveReport:
     final_residual: float
     device_seconds: float
     wall_seconds: float
+    used_graph: bool = False
+    graph_error: int = 0
 
 
 @dataclass
@@ -334,7 +337,8 @@ class Hierarchy:
             raise DivergedError(rep.iterations, lib().mpmg_last_error().decode())
         _check(rc, "ir_solve")
         return u, SolveReport(bool(rep.converged), rep.iterations, hist[: rep.iterations + 1].copy(),
-                              rep.final_residual, rep.device_seconds, rep.wall_seconds)
+                              rep.final_residual, rep.device_seconds, rep.wall_seconds, bool(rep.used_graph),
+                              rep.graph_error)
 
     def ir_solve_ptr(self, b_ptr, u_ptr, config: IrConfig = None, device=False):
         """ir_solve on raw pointers (host pinned buffers, or device padded
@@ -348,4 +352,4 @@ class Hierarchy:
             raise DivergedError(rep.iterations, lib().mpmg_last_error().decode())
         _check(rc, "ir_solve")
         return SolveReport(bool(rep.converged), rep.iterations, np.zeros(0), rep.final_residual,
-                           rep.device_seconds, rep.wall_seconds)
+                           rep.device_seconds, rep.wall_seconds, bool(rep.used_graph), rep.graph_error)

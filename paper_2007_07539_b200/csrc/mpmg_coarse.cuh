@@ -1,0 +1,638 @@
+#pragma once
+// Coarse part of the V-cycle in ONE persistent cooperative launch: every
+// level with <= kCoarsePoints interior unknowns (127^3 / 1447^2 and below:
+// the levels whose per-launch work is too small to hide a kernel launch and
+// a pipeline ramp) runs inside a single grid -- pre-smoothing, defect,
+// restriction (with the DSH rescale), the CG base solve on level 0,
+// prolongation + correction and post-smoothing -- separated by grid-wide
+// barriers instead of kernel launches. Levels with <= kCtaPoints unknowns
+// are worked by CTA 0 alone out of shared memory with __syncthreads; the
+// other CTAs wait at the next grid barrier. This replaces the coarse part of
+// the reference's recursion (cycle_at, multigrid.cpp:362-393) and cg_solve
+// (multigrid.cpp:91-151).
+//
+// Arithmetic is the same per-operation rounding as the streaming kernels
+// (policy as template parameters). The grid levels live in global memory
+// (L2-resident at these sizes; grid.sync() orders and publishes the writes
+// of one step to the next). Reductions the reference accumulates
+// sequentially (dot_fp64 / norm2_fp64, kernels.cpp:368-395; the DSH
+// restriction norm, multigrid.cpp:246-250) run on one thread in the
+// reference's lexicographic order, so the base solve is bitwise identical to
+// the reference.
+#include <cooperative_groups.h>
+
+#include <type_traits>
+
+#include "mpmg_arith.cuh"
+#include "mpmg_internal.h"
+
+#include <algorithm>
+
+namespace mpmg_impl {
+
+using namespace mpmg_dev;
+
+namespace coarse_detail {
+
+constexpr int kThreads = 512;
+constexpr int kCtaPoints = 4096;
+
+template <int PR> struct T_;
+template <> struct T_<P16> { using T = __half; };
+template <> struct T_<P32> { using T = float; };
+template <> struct T_<P64> { using T = double; };
+
+// loads of data written earlier in this launch (plain loads: grid.sync()
+// and __syncthreads order them after the writes)
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) { return *p; }
+
+template <int PR, bool FTZ, bool FMA, bool ACC32>
+struct Lv {
+  using T = typename T_<PR>::T;
+  static __device__ __forceinline__ T from(double v) {
+    if constexpr (PR == P16) return round16<FTZ>(v);
+    else if constexpr (PR == P32) return round32<FTZ>(v);
+    else return v;
+  }
+  static __device__ __forceinline__ double wide(T v) {
+    if constexpr (PR == P16) return (double)__half2float(v);
+    else return (double)v;
+  }
+  static __device__ __forceinline__ T zero() { return T(0); }
+  static __device__ __forceinline__ T fma(T a, T b, T c) {
+    if constexpr (PR == P16) return fma16s<FTZ, FMA>(a, b, c);
+    else if constexpr (PR == P32) return fma32<FTZ, FMA>(a, b, c);
+    else return fma64<FMA>(a, b, c);
+  }
+  static __device__ __forceinline__ T mul(T a, T b) {
+    if constexpr (PR == P16) return mul16s<FTZ>(a, b);
+    else if constexpr (PR == P32) return mul32<FTZ>(a, b);
+    else return mul64(a, b);
+  }
+  // transfer weight 2^-k, exact in the compute precision (no conversion)
+  static __device__ __forceinline__ T weight(int k) {
+    if constexpr (PR == P16) return __ushort_as_half((unsigned short)(0x3C00 - (k << 10)));
+    else if constexpr (PR == P32) return __int_as_float(0x3F800000 - (k << 23));
+    else return __longlong_as_double(0x3FF0000000000000LL - ((long long)k << 52));
+  }
+  // transfer_product step (multigrid.cpp:166-195): FP32 unfused flushes only the sum
+  static __device__ __forceinline__ T xfer(T w, T x, T acc) {
+    if constexpr (PR == P32) return f32<FTZ>(FMA ? __fmaf_rn(w, x, acc) : __fadd_rn(__fmul_rn(w, x), acc));
+    else return fma(w, x, acc);
+  }
+  // the level's taps in the compute precision, converted once per operation
+  struct Taps {
+    T t[27];
+    float f[27];
+  };
+  // (t16/t32: the level's taps pre-rounded once per launch in shared memory)
+  static __device__ __forceinline__ Taps taps(const CoarseLevel& L, const __half* t16, const float* t32) {
+    Taps k;
+#pragma unroll
+    for (int t = 0; t < 27; ++t) {
+      if constexpr (PR == P16) k.t[t] = t16[t];
+      else if constexpr (PR == P32) k.t[t] = t32[t];
+      else k.t[t] = L.taps[t];
+      k.f[t] = t32[t];
+    }
+    return k;
+  }
+  // A x at padded index i (all 3^dim taps in slot order; ghosts are zero)
+  template <int DIM>
+  static __device__ __forceinline__ T apply_d(const Taps& k, const T* x, int i, int P) {
+    const int pl = DIM == 3 ? P * P : 0;
+    if constexpr (PR == P16 && ACC32) {  // Fp16Accum::FP32 (kernels.cpp:151-162)
+      float acc = 0.0f;
+      int t = 0;
+#pragma unroll
+      for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx, ++t)
+            acc = fma32<FTZ, FMA>(k.f[t], __half2float(ldcg(x + i + dz * pl + dy * P + dx)), acc);
+      return f16s<FTZ>(__float2half_rn(acc));
+    } else {
+      T acc = zero();
+      int t = 0;
+#pragma unroll
+      for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx, ++t) acc = fma(k.t[t], ldcg(x + i + dz * pl + dy * P + dx), acc);
+      return acc;
+    }
+  }
+  static __device__ __forceinline__ T apply(const Taps& k, int dim, const T* x, int i, int P) {
+    return dim == 3 ? apply_d<3>(k, x, i, P) : apply_d<2>(k, x, i, P);
+  }
+};
+
+struct Pt {
+  int n, m, P, dim;
+  unsigned magic;  // ceil(2^32 / m): k / m == umulhi(k, magic) for k < 2^32 / m
+  __device__ __forceinline__ int idx(int k) const {  // compact k -> padded index
+    const unsigned q = __umulhi((unsigned)k, magic);
+    const int x = k - (int)q * m + 1;
+    if (dim == 2) return ((int)q + 1) * P + x;
+    const unsigned z = __umulhi(q, magic);
+    return (((int)z + 1) * P + (int)(q - z * m) + 1) * P + x;
+  }
+};
+
+__device__ __forceinline__ Pt points(const CoarseLevel& L) {
+  Pt p;
+  p.P = L.nodes - 1;
+  p.m = p.P - 1;
+  p.dim = L.dim;
+  p.n = L.dim == 3 ? p.m * p.m * p.m : p.m * p.m;
+  p.magic = 0xFFFFFFFFu / (unsigned)p.m + 1u;
+  return p;
+}
+
+__device__ __forceinline__ void grid_sync() { cooperative_groups::this_grid().sync(); }
+
+// UP: the one precision of every level (P16/P32/P64: H_MG, D_MG -- a single
+// code path, a third of the instruction footprint), or 3 for mixed cascades
+template <bool FTZ, bool FMA, bool ACC32, int UP>
+struct Coarse {
+  const CoarseArgs& a;
+  unsigned rank, ncta;
+  CoarseLevel* lv;  // level table in shared memory: CTA 0's small levels point into shared memory
+  void* const* cgp;  // CG scratch r, p, ap, s, best
+  const __half (*t16)[27];
+  const float (*t32)[27];
+  __device__ Coarse(const CoarseArgs& args, CoarseLevel* table, void* const* cg, const __half (*a16)[27],
+                    const float (*a32)[27])
+      : a(args), rank(blockIdx.x), ncta(gridDim.x), lv(table), cgp(cg), t16(a16), t32(a32) {}
+  template <int PR>
+  __device__ typename Lv<PR, FTZ, FMA, ACC32>::Taps taps_of(const CoarseLevel& L) const {
+    const int l = (int)(&L - lv);
+    return Lv<PR, FTZ, FMA, ACC32>::taps(L, t16[l], t32[l]);
+  }
+
+  template <int PR> using O = Lv<PR, FTZ, FMA, ACC32>;
+
+  __device__ bool small(const CoarseLevel& L) const { return points(L).n <= a.cta_points; }
+  long long t0 = 0;
+  int nst = 0;
+  // phase timestamps (MPMG_COARSE_DEBUG): code*1e12 + cycles since start,
+  // kept in registers by thread 0 of CTA 0 and written to a.dbg at the end
+  __device__ void stamp(int code, int l) {
+    if (a.dbg && rank == 0 && threadIdx.x == 0 && nst < 63)
+      a.dbg[1 + nst++] = (long long)(code * 100 + l) * 1000000000000LL + (clock64() - t0);
+  }
+  __device__ void stamps_done() {
+    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[0] = nst;
+  }
+  // team of a level: the whole grid, or CTA 0 alone
+  __device__ bool in_team(const CoarseLevel& L) const { return !small(L) || rank == 0; }
+  __device__ void sync(const CoarseLevel& L) {
+    if (small(L)) __syncthreads();
+    else grid_sync();
+  }
+
+  template <typename F>
+  __device__ void for_points(const CoarseLevel& L, F&& f) {
+    const Pt p = points(L);
+    int start = threadIdx.x, stride = blockDim.x;
+    if (!small(L)) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
+    for (int k = start; k < p.n; k += stride) f(p.idx(k), p.P);
+  }
+
+  template <typename F>
+  __device__ void by_prec(int prec, F&& f) {
+    if constexpr (UP < 3) {
+      (void)prec;
+      f(std::integral_constant<int, UP>{});
+    } else {
+      if (prec == MPMG_FP16) f(std::integral_constant<int, P16>{});
+      else if (prec == MPMG_FP32) f(std::integral_constant<int, P32>{});
+      else f(std::integral_constant<int, P64>{});
+    }
+  }
+
+  template <int PR>
+  __device__ void jacobi(const CoarseLevel& L, const void* bv, const void* uin, void* uout, bool from_zero) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    const T* b = static_cast<const T*>(bv);
+    const T* u = static_cast<const T*>(uin);
+    T* o = static_cast<T*>(uout);
+    const T w = OP::from(L.omega), d = OP::from(L.inv_diag), m1 = OP::from(-1.0);
+    const auto tk = taps_of<PR>(L);
+    for_points(L, [&](int i, int P) {
+      const T t = from_zero ? OP::zero() : OP::apply(tk, L.dim, u, i, P);
+      const T r = OP::fma(m1, t, ldcg(b + i));
+      o[i] = OP::fma(w, OP::mul(d, r), from_zero ? OP::zero() : ldcg(u + i));
+    });
+  }
+
+  template <int PR>
+  __device__ void defect(const CoarseLevel& L, const void* bv, const void* uv, void* rv) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    const T m1 = OP::from(-1.0);
+    const auto tk = taps_of<PR>(L);
+    for_points(L, [&](int i, int P) {
+      static_cast<T*>(rv)[i] = OP::fma(m1, OP::apply(tk, L.dim, static_cast<const T*>(uv), i, P), ldcg(static_cast<const T*>(bv) + i));
+    });
+  }
+
+  // R r_f (product in the fine precision FP) -> coarse b; when `keep`, the
+  // binary64 products go to C.prod first (DSH rescale norm)
+  template <int FP>
+  __device__ void restrict_to(const CoarseLevel& F, const CoarseLevel& C, const void* rfv, bool keep) {
+    using OF = O<FP>;
+    using T = typename OF::T;
+    const T* rf = static_cast<const T*>(rfv);
+    const int Pf = F.nodes - 1;
+    const int pf = F.dim == 3 ? Pf * Pf : 0;
+    for_points(C, [&](int ci, int Pc) {
+      const int cx = ci % Pc, cy = (ci / Pc) % Pc, cz = F.dim == 3 ? ci / (Pc * Pc) : 0;
+      const int cf = cz * 2 * pf + cy * 2 * Pf + cx * 2;
+      T acc = OF::zero();
+      for (int dz = (F.dim == 3 ? -1 : 0); dz <= (F.dim == 3 ? 1 : 0); ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            acc = OF::xfer(OF::weight((dx != 0) + (dy != 0) + (dz != 0)), ldcg(rf + cf + dz * pf + dy * Pf + dx), acc);
+          }
+      if (keep) C.prod[ci] = OF::wide(acc);
+      else by_prec(C.prec, [&](auto cp) {
+        using OC = O<decltype(cp)::value>;
+        static_cast<typename OC::T*>(C.b)[ci] = OC::from(OF::wide(acc));  // scale 1
+      });
+    });
+  }
+
+  template <int CPc>
+  __device__ void restrict_store(const CoarseLevel& C, double scale) {
+    using OC = O<CPc>;
+    for_points(C, [&](int ci, int) {
+      static_cast<typename OC::T*>(C.b)[ci] = OC::from(C.prod[ci] / scale);
+    });
+  }
+
+  // u_f += round_f(scale * P c) (product in the coarse precision)
+  template <int FP, int CPc>
+  __device__ void prolong(const CoarseLevel& F, const CoarseLevel& C, const void* ccv, void* ufv, double scale) {
+    using OC = O<CPc>;
+    using OF = O<FP>;
+    using TC = typename OC::T;
+    using TF = typename OF::T;
+    const TC* cc = static_cast<const TC*>(ccv);
+    TF* uf = static_cast<TF*>(ufv);
+    const int Pc = C.nodes - 1;
+    for_points(F, [&](int fi, int Pf) {
+      const int fx = fi % Pf, fy = (fi / Pf) % Pf, fz = F.dim == 3 ? fi / (Pf * Pf) : 0;
+      const int nx = (fx & 1) ? 2 : 1, ny = (fy & 1) ? 2 : 1, nz = F.dim == 3 ? ((fz & 1) ? 2 : 1) : 1;
+      const int px[2] = {fx >> 1, (fx + 1) >> 1}, py[2] = {fy >> 1, (fy + 1) >> 1}, pz[2] = {fz >> 1, (fz + 1) >> 1};
+      const TC w = OC::weight((fx & 1) + (fy & 1) + (F.dim == 3 ? (fz & 1) : 0));
+      TC acc = OC::zero();
+      for (int c = 0; c < nz; ++c)
+        for (int b = 0; b < ny; ++b)
+          for (int aa = 0; aa < nx; ++aa) {
+            const int ci = (F.dim == 3 ? pz[c] * Pc * Pc : 0) + py[b] * Pc + px[aa];
+            acc = OC::xfer(w, ldcg(cc + ci), acc);
+          }
+      const TF t = OF::from(OC::wide(acc) * scale);
+      uf[fi] = OF::fma(OF::from(1.0), t, ldcg(uf + fi));
+    });
+  }
+
+  // sequential fma dot in lexicographic interior order (kernels.cpp:368-382)
+  template <typename TA, typename TB>
+  __device__ double dot_seq(const Pt& p, const TA* x, const TB* y) {
+    double acc = 0.0;
+    for (int k = 0; k < p.n; ++k) {
+      const int i = p.idx(k);
+      acc = __fma_rn((double)wide_v(ldcg(x + i)), (double)wide_v(ldcg(y + i)), acc);
+    }
+    return acc;
+  }
+  template <typename T>
+  static __device__ __forceinline__ double wide_v(T v) {
+    if constexpr (std::is_same<T, __half>::value) return (double)__half2float(v);
+    else return (double)v;
+  }
+
+  // CG on level 0 (multigrid.cpp:91-151), CTA 0 only
+  template <int PR>
+  __device__ void cg(const CoarseLevel& L, const void* bv, void* uv) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    __shared__ double sh;
+    const T* b = static_cast<const T*>(bv);
+    T* u = static_cast<T*>(uv);
+    T* r = static_cast<T*>(cgp[0]);
+    T* p = static_cast<T*>(cgp[1]);
+    T* ap = static_cast<T*>(cgp[2]);
+    T* sc = static_cast<T*>(cgp[3]);
+    T* best = static_cast<T*>(cgp[4]);
+    const Pt pt = points(L);
+    auto dot = [&](const T* x, const T* y) -> double {
+      __syncthreads();
+      if (threadIdx.x == 0) sh = dot_seq(pt, x, y);
+      __syncthreads();
+      const double v = sh;
+      __syncthreads();
+      return v;
+    };
+    auto each = [&](auto&& f) {
+      for (int k = threadIdx.x; k < pt.n; k += blockDim.x) f(pt.idx(k));
+      __syncthreads();
+    };
+    const int max_it = a.base_maxit > 0 ? a.base_maxit : 10 * pt.n;
+    each([&](int i) {
+      u[i] = OP::zero();
+      r[i] = ldcg(b + i);
+      p[i] = ldcg(b + i);
+      best[i] = OP::zero();
+    });
+    const double norm_b = sqrt(dot(b, b));
+    if (norm_b == 0.0) return;
+    const double thr = a.base_mode == 0 ? a.base_tol * norm_b : a.base_tol;
+    double rz = dot(r, r);
+    double true_res = norm_b, best_res = norm_b;
+    int it = 0;
+    const T m1 = OP::from(-1.0);
+    const auto tk = taps_of<PR>(L);
+    while (true_res >= thr && it < max_it) {
+      each([&](int i) { ap[i] = OP::apply(tk, L.dim, p, i, pt.P); });
+      const double pAp = dot(p, ap);
+      if (!(pAp > 0.0) || !isfinite(pAp)) break;
+      const double alpha = rz / pAp;
+      const T al = OP::from(alpha), mal = OP::from(-alpha);
+      each([&](int i) {
+        u[i] = OP::fma(al, ldcg(p + i), ldcg(u + i));
+        r[i] = OP::fma(mal, ldcg(ap + i), ldcg(r + i));
+      });
+      const double rz_new = dot(r, r);
+      ++it;
+      each([&](int i) { sc[i] = OP::apply(tk, L.dim, u, i, pt.P); });
+      each([&](int i) { sc[i] = OP::fma(m1, ldcg(sc + i), ldcg(b + i)); });
+      true_res = sqrt(dot(sc, sc));
+      if (true_res < best_res) {
+        best_res = true_res;
+        each([&](int i) { best[i] = ldcg(u + i); });
+      }
+      if (rz == 0.0) break;
+      const T be = OP::from(rz_new / rz);
+      each([&](int i) { p[i] = OP::fma(be, ldcg(p + i), ldcg(r + i)); });
+      rz = rz_new;
+    }
+    if (true_res > best_res) each([&](int i) { u[i] = ldcg(best + i); });
+    if (threadIdx.x == 0 && a.cg_iterations) *a.cg_iterations = it;
+  }
+
+  __device__ void copy_level(const CoarseLevel& L, const void* src, void* dst) {
+    for_points(L, [&](int i, int) {
+      if (L.prec == MPMG_FP16) static_cast<uint16_t*>(dst)[i] = static_cast<const uint16_t*>(src)[i];
+      else if (L.prec == MPMG_FP32) static_cast<uint32_t*>(dst)[i] = static_cast<const uint32_t*>(src)[i];
+      else static_cast<uint64_t*>(dst)[i] = static_cast<const uint64_t*>(src)[i];
+    });
+  }
+
+  // ping-pong smoothing between L.u and L.u2; returns the result buffer
+  __device__ void* smooth(const CoarseLevel& L, void* cur, int steps) {
+    for (int s = 0; s < steps; ++s) {
+      void* out = (cur == L.u) ? L.u2 : L.u;
+      const bool z = cur == nullptr;
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { jacobi<decltype(pc)::value>(L, L.b, z ? L.b : cur, out, z); });
+      sync(L);
+      cur = out;
+    }
+    return cur;
+  }
+
+  // Every CTA walks the same schedule; an op on a small level is worked by
+  // CTA 0 only and followed by __syncthreads, an op on a big level by the
+  // whole grid and followed by a grid barrier. The one extra grid
+  // barrier before prolongating a small level's correction into a big level
+  // publishes CTA 0's small-level results.
+  int entry = -1;  // highest level worked by CTA 0 alone (its b arrives in global memory)
+
+  // global b of the entry level -> CTA 0's shared copy
+  __device__ void stage_in(int l) {
+    if (rank == 0) copy_level(lv[l], a.lv[l].b, lv[l].b);
+    __syncthreads();
+  }
+  __device__ void stage_out(int l, const void* src) {
+    if (rank == 0) copy_level(lv[l], src, a.lv[l].u);
+    __syncthreads();
+  }
+
+  __device__ void run() {
+    __shared__ double scales[kMaxCoarseLevels];
+    void* cur[kMaxCoarseLevels];
+    const int top = a.nlev - 1;
+    t0 = clock64();
+    for (int l = top; l >= 0; --l)
+      if (small(lv[l])) { entry = l; break; }
+    // down-sweep (cycle_at before the recursive call)
+    for (int l = top; l >= 1; --l) {
+      const CoarseLevel& L = lv[l];
+      const CoarseLevel& C = lv[l - 1];
+      stamp(1, l);
+      if (small(L) && l == entry) stage_in(l);
+      void* u = smooth(L, nullptr, a.pre);
+      if (u == nullptr) {  // pre_steps == 0: u = 0
+        if (in_team(L)) for_points(L, [&](int i, int) {
+          if (L.prec == MPMG_FP16) static_cast<uint16_t*>(L.u)[i] = 0;
+          else if (L.prec == MPMG_FP32) static_cast<float*>(L.u)[i] = 0.f;
+          else static_cast<double*>(L.u)[i] = 0.0;
+        });
+        sync(L);
+        u = L.u;
+      }
+      cur[l] = u;
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { defect<decltype(pc)::value>(L, L.b, u, L.r); });
+      sync(L);
+      const bool rescale = a.rescale && C.prec == MPMG_FP16;  // multigrid.cpp:383
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { restrict_to<decltype(pc)::value>(L, C, L.r, rescale); });
+      sync(L);
+      if (threadIdx.x == 0) {
+        double sc = 1.0;
+        if (rescale && in_team(L)) {  // multigrid.cpp:246-250, sequential fma order
+          const Pt pc = points(C);
+          double acc = 0.0;
+          for (int k = 0; k < pc.n; ++k) {
+            const double v = C.prod[pc.idx(k)];
+            acc = __fma_rn(v, v, acc);
+          }
+          const double nrm = sqrt(acc);
+          if (nrm > 0.0 && isfinite(nrm)) sc = nrm;
+        }
+        scales[l - 1] = sc;
+      }
+      __syncthreads();
+      if (rescale) {
+        if (in_team(L)) by_prec(C.prec, [&](auto cp) { restrict_store<decltype(cp)::value>(C, scales[l - 1]); });
+        sync(L);
+      }
+    }
+    // base solve on CTA 0
+    if (top == 0 && entry == 0) {
+      // single-level call (OP_COARSE_SOLVE): result to global
+      stage_in(0);
+      if (rank == 0) by_prec(lv[0].prec, [&](auto pc) { cg<decltype(pc)::value>(lv[0], lv[0].b, lv[0].u); });
+      __syncthreads();
+      if (rank == 0) copy_level(lv[0], lv[0].u, a.lv[0].u);
+      __syncthreads();
+      return;
+    }
+    {
+      const CoarseLevel& B = lv[0];
+      if (entry == 0) stage_in(0);
+      if (rank == 0) by_prec(B.prec, [&](auto pc) { cg<decltype(pc)::value>(B, B.b, B.u); });
+      __syncthreads();
+      if (!small(B)) grid_sync();
+      cur[0] = B.u;
+      stamp(2, 0);
+    }
+    // up-sweep
+    for (int l = 1; l <= top; ++l) {
+      const CoarseLevel& L = lv[l];
+      const CoarseLevel& C = lv[l - 1];
+      if (!small(L) && small(C)) {
+        stage_out(l - 1, cur[l - 1]);  // CTA 0's shared-memory correction -> global
+        cur[l - 1] = a.lv[l - 1].u;
+        grid_sync();
+      }
+      if (in_team(L)) {
+        by_prec(L.prec, [&](auto fp) {
+          by_prec(C.prec, [&](auto cp) {
+            prolong<decltype(fp)::value, decltype(cp)::value>(L, C, cur[l - 1], cur[l], scales[l - 1]);
+          });
+        });
+      }
+      sync(L);
+      void* u = smooth(L, cur[l], a.post);
+      if (l == top && u != a.lv[top].u) {  // the caller reads the top correction from global L.u
+        if (in_team(L)) copy_level(L, u, a.lv[top].u);
+        sync(L);
+        u = a.lv[top].u;
+      }
+      cur[l] = u;
+      stamp(3, l);
+    }
+    stamps_done();
+  }
+};
+
+__host__ __device__ inline long long padded_of(const CoarseLevel& L) {
+  const long long P = L.nodes - 1;
+  return L.dim == 3 ? P * P * P + P * P + P + 1 : P * P + P + 1;
+}
+__host__ __device__ inline int bytes_of(int prec) { return prec == MPMG_FP16 ? 2 : (prec == MPMG_FP32 ? 4 : 8); }
+__host__ __device__ inline bool small_level(const CoarseLevel& L, int cta_points) {
+  const long long m = L.nodes - 2;
+  return (L.dim == 3 ? m * m * m : m * m) <= cta_points;
+}
+
+// shared bytes for CTA 0's small levels (u, u2, b, r each, 16-byte aligned)
+// plus the CG scratch of level 0
+__host__ __device__ inline size_t coarse_smem(const CoarseArgs& a) {
+  size_t n = 0;
+  for (int l = 0; l < a.nlev; ++l)
+    if (small_level(a.lv[l], a.cta_points)) n += 4 * ((padded_of(a.lv[l]) * bytes_of(a.lv[l].prec) + 15) / 16 * 16);
+  if (small_level(a.lv[0], a.cta_points)) n += 5 * ((padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16);
+  return n;
+}
+
+template <bool FTZ, bool FMA, bool ACC32, int UP>
+__global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a, int use_smem) {
+  __shared__ CoarseLevel table[kMaxCoarseLevels];
+  __shared__ __half t16[kMaxCoarseLevels][27];
+  __shared__ float t32[kMaxCoarseLevels][27];
+  for (int i = threadIdx.x; i < a.nlev * 27; i += blockDim.x) {
+    const double v = a.lv[i / 27].taps[i % 27];
+    t16[i / 27][i % 27] = round16<FTZ>(v);
+    t32[i / 27][i % 27] = round32<FTZ>(v);
+  }
+  __shared__ void* cg[5];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  if (threadIdx.x == 0) {
+    for (int l = 0; l < a.nlev; ++l) table[l] = a.lv[l];
+    cg[0] = a.cg_r; cg[1] = a.cg_p; cg[2] = a.cg_ap; cg[3] = a.cg_s; cg[4] = a.cg_best;
+    if (use_smem && blockIdx.x == 0) {
+      unsigned char* p = dyn;
+      for (int l = 0; l < a.nlev; ++l) {
+        if (!small_level(a.lv[l], a.cta_points)) continue;
+        const size_t b = (padded_of(a.lv[l]) * bytes_of(a.lv[l].prec) + 15) / 16 * 16;
+        table[l].u = p; p += b;
+        table[l].u2 = p; p += b;
+        table[l].b = p; p += b;
+        table[l].r = p; p += b;
+      }
+      if (small_level(a.lv[0], a.cta_points)) {
+        const size_t b = (padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16;
+        for (int k = 0; k < 5; ++k) { cg[k] = p; p += b; }
+      }
+    }
+  }
+  __syncthreads();
+  if (use_smem && blockIdx.x == 0) {  // ghosts must read as zero
+    const size_t n = coarse_smem(a) / 16;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32);
+  c.run();
+}
+
+template <bool FTZ, bool FMA, bool ACC32, int UP>
+cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
+  auto kern = k_coarse<FTZ, FMA, ACC32, UP>;
+  const size_t smem = coarse_smem(a);
+  const int use_smem = smem <= 200 * 1024 ? 1 : 0;
+  const size_t dyn = use_smem ? smem : 0;
+  static size_t attr_set = 0;
+  if (use_smem && smem > attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = smem;
+  }
+  // grid: every co-resident CTA when the top level is a grid level, else one
+  const CoarseLevel& T = a.lv[a.nlev - 1];
+  unsigned grid = 1;
+  if (!small_level(T, a.cta_points)) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+    grid = (unsigned)std::max(1, per) * (unsigned)std::max(1, sms);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, use_smem);
+}
+
+template <bool FTZ, bool FMA, bool ACC32>
+cudaError_t launch_t(const CoarseArgs& a, cudaStream_t s) {
+  bool uni = true;
+  for (int l = 1; l < a.nlev; ++l) uni = uni && a.lv[l].prec == a.lv[0].prec;
+  if (!uni) return launch_u<FTZ, FMA, ACC32, 3>(a, s);
+  switch (a.lv[0].prec) {
+    case MPMG_FP16: return launch_u<FTZ, FMA, ACC32, P16>(a, s);
+    case MPMG_FP32: return launch_u<FTZ, FMA, ACC32, P32>(a, s);
+    default: return launch_u<FTZ, FMA, ACC32, P64>(a, s);
+  }
+}
+
+}  // namespace coarse_detail
+
+// one translation unit per FTZ policy (mpmg_coarse_ftz0.cu / _ftz1.cu)
+cudaError_t launch_coarse_ftz0(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
+cudaError_t launch_coarse_ftz1(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
+
+}  // namespace mpmg_impl

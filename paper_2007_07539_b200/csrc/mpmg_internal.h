@@ -26,6 +26,8 @@ double fp16_value(uint16_t bits);
 // level ops: op in {0 spmv, 1 defect, 2 jacobi}; level precision A.prec
 cudaError_t launch_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                             uint32_t policy, cudaStream_t s);
+cudaError_t launch_jacobi_zero2(const mpmg_stencil& A, const void* b, void* tmp, void* out, double omega,
+                                double omega_r, uint32_t policy, cudaStream_t s);
 cudaError_t launch_level_op_f16(int op, const mpmg_stencil& A, const void* x, const void* b, void* out,
                                 double omega, uint32_t policy, cudaStream_t s);
 cudaError_t launch_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out,
@@ -104,6 +106,9 @@ struct CoarseArgs {
   // CG scratch on level 0 (padded, level-0 precision) + best iterate
   void *cg_r, *cg_p, *cg_ap, *cg_s, *cg_best;
   int* cg_iterations;  // optional diagnostics (device)
+  int cta_points;      // levels with <= this many unknowns run on CTA 0 out of shared memory
+  int debug;           // MPMG_COARSE_DEBUG=1: record per-phase clock64 stamps
+  long long* dbg;      // device buffer for them (64 entries) or nullptr
 };
 cudaError_t launch_coarse_cycle(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
 

@@ -71,6 +71,22 @@ bool stencil_supported(int dim, int nodes, int prec) {
   return P >= 16 && P % W == 0;
 }
 
+// two Jacobi steps from u = 0 (steps 1+2 of the pre-smoother, multigrid.cpp:
+// 376-377): one fused plane-kernel pass over b when covered, else the
+// pointwise first step into `tmp` followed by a streaming step
+cudaError_t launch_jacobi_zero2(const mpmg_stencil& A, const void* b, void* tmp, void* out, double omega,
+                                double omega_r, uint32_t policy, cudaStream_t s) {
+  cudaError_t pe = cudaSuccess;
+  bool done = false;
+  if (A.prec == MPMG_FP16) done = plane_level_op_f16(3, A, b, b, out, omega, policy, s, &pe);
+  else if (A.prec == MPMG_FP32) done = plane_level_op_f32(3, A, b, b, out, omega, policy, s, &pe);
+  else done = plane_level_op_f64(3, A, b, b, out, omega, policy, s, &pe);
+  if (done) return pe;
+  cudaError_t e = launch_jacobi_zero(A.dim, A.nodes, A.prec, b, tmp, omega_r, A.inv_diag, policy, s);
+  if (e == cudaSuccess) e = launch_level_op(2, A, tmp, b, out, omega, policy, s);
+  return e;
+}
+
 cudaError_t launch_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                             uint32_t policy, cudaStream_t s) {
   switch (A.prec) {

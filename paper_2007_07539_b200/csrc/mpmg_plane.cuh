@@ -34,7 +34,8 @@
 
 namespace mpmg_dev {
 
-enum { POP_SPMV = 0, POP_DEFECT = 1, POP_JACOBI = 2, POP_DEFECT64 = 3, POP_RESNORM = 4, POP_UPDATE = 5 };
+enum { POP_SPMV = 0, POP_DEFECT = 1, POP_JACOBI = 2, POP_DEFECT64 = 3, POP_RESNORM = 4, POP_UPDATE = 5,
+       POP_JACOBI_Z = 6 };  // JACOBI_Z: steps 1 and 2 from u = 0 fused (operand = b, u1 = w D^-1 b on the fly)
 
 struct PlaneArgs {
   int P;             // pitch
@@ -398,6 +399,21 @@ __device__ __forceinline__ Row<EP, W> emul(TT a, const Row<EP, W>& x) {
   }
   return r;
 }
+// first Jacobi step from zero, elementwise: u1 = fma(w, d*b, +0) (the
+// fused form of t = A*0, r = b - t, t = d r, u = 0 + w t; multigrid.cpp:79-89)
+template <int CP, bool FTZ, bool FMA, int W, typename TT>
+__device__ __forceinline__ void jz_row(TT d, TT w, Row<CP, W>& x) {
+  Row<CP, W> zero;
+  rzero(zero);
+  x = efma<CP, FTZ, FMA, W>(w, emul<CP, FTZ, W>(d, x), zero);
+}
+template <int CP, bool FTZ, bool FMA, typename ST, typename TT>
+__device__ __forceinline__ ST jz_scalar(TT d, TT w, ST v) {
+  if constexpr (CP == P16) return fma16s<FTZ, FMA>(__low2half(w), mul16s<FTZ>(__low2half(d), v), __ushort_as_half((unsigned short)0));
+  else if constexpr (CP == P32) return fma32<FTZ, FMA>(w, mul32<FTZ>(d, v), 0.0f);
+  else return fma64<FMA>(w, mul64(d, v), 0.0);
+}
+
 // binary32 accumulators -> binary16 (Fp16Accum::FP32, kernels.cpp:160-161)
 template <bool FTZ, int W>
 __device__ __forceinline__ Row<P16, W> quant16(const Row<P32, W>& a) {
@@ -418,7 +434,9 @@ __device__ __forceinline__ bool is_face(int k) {
 // LP storage precision of the stencil operand; CP accumulation precision;
 // EP epilogue/output precision; W values per lane; WX warps per row;
 // WY warp-rows per CTA; RY rows per thread; NS pipeline stages.
-template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, bool SKIPF, int W, int WX, int WY, int RY, int NS>
+// OPT bit 0: stage b through shared memory (instead of the register prefetch)
+template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, bool SKIPF, int W, int WX, int WY, int RY, int NS,
+          int OPT = 0>
 struct PlaneK {
   static constexpr int kThreads = 32 * WX * WY;
   static constexpr int TY = WY * RY;
@@ -426,7 +444,8 @@ struct PlaneK {
   static constexpr bool kNorm = OP == POP_DEFECT64 || OP == POP_RESNORM || OP == POP_UPDATE;
   // binary16/32 level ops prefetch b into registers one plane ahead (global
   // loads); the FP64 epilogue operands are staged through shared memory
-  static constexpr bool kBReg = (OP == POP_DEFECT || OP == POP_JACOBI) && EP != P64;
+  static constexpr bool kBReg = (OP == POP_DEFECT || OP == POP_JACOBI) && EP != P64 && !(OPT & 1);
+  static constexpr bool kJZ = OP == POP_JACOBI_Z;  // b is the stencil operand: nothing else staged
   static constexpr int kEpiBytes = OP == POP_UPDATE ? 16 : ((kB && !kBReg) ? Bytes<EP>::v : 0);  // per value
   static constexpr int kP = 32 * WX * W;  // pitch (compile-time)
   static constexpr int kXRow = kP * Bytes<LP>::v;
@@ -436,9 +455,10 @@ struct PlaneK {
   static constexpr int kSmem = 128 + NS * kStage;
 };
 
-template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, bool SKIPF, int W, int WX, int WY, int RY, int NS>
+template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, bool SKIPF, int W, int WX, int WY, int RY, int NS,
+          int OPT = 0>
 __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ PlaneArgs a) {
-  using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, W, WX, WY, RY, NS>;
+  using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, W, WX, WY, RY, NS, OPT>;
   using ST = typename Sc<CP>::T;
   constexpr int P = K::kP;
   constexpr int TY = K::TY;
@@ -503,6 +523,18 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
 #pragma unroll
     for (int k = 0; k < 27; ++k) tk[k] = (SKIPF && is_face(k)) ? 0u : s_taps[k];
   }
+  // JACOBI_Z: D^-1 and omega in the compute precision
+  const auto jd = [&] {
+    if constexpr (CP == P16) return a.d16;
+    else if constexpr (CP == P32) return a.d32;
+    else return a.d64;
+  }();
+  const auto jw = [&] {
+    if constexpr (CP == P16) return a.w16;
+    else if constexpr (CP == P32) return a.w32;
+    else return a.w64;
+  }();
+  (void)jd; (void)jw;
   auto tapk = [&](int k) {
     if constexpr (CP == P16) return u2h(tk[k]);
     else return tap<CP>(a, k);
@@ -537,11 +569,16 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
       const unsigned char* rp = st + (tr + j) * K::kXRow;
       Row<CP, W> c, L, R;
       rload<LP, CP, W>(rp + x0 * Bytes<LP>::v, c);
+      if constexpr (K::kJZ) jz_row<CP, FTZ, FMA, W>(jd, jw, c);
       ST prev = shup(rlast<CP, W>(c));
       ST next = shdn(rfirst<CP, W>(c));
       if constexpr (WX > 1) {
         if (lane == 0) prev = x0 > 0 ? sload_s<LP, CP>(rp + (x0 - 1) * Bytes<LP>::v) : ST(0);
         if (lane == 31) next = x0 + W < P ? sload_s<LP, CP>(rp + (x0 + W) * Bytes<LP>::v) : ST(0);
+        if constexpr (K::kJZ) {
+          prev = jz_scalar<CP, FTZ, FMA, ST>(jd, jw, prev);
+          next = jz_scalar<CP, FTZ, FMA, ST>(jd, jw, next);
+        }
       } else {
         if (lane == 0) prev = ST(0);   // x = -1: only feeds the ghost output x = 0
         if (lane == 31) next = ST(0);  // x = P: the aliased ghost (zero)
@@ -582,9 +619,10 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
       if constexpr (OP == POP_SPMV) {
         if (x0 == 0) rzero_first<EP, W>(t);
         if (v) gstore<EP, W>(a.out, gi, t);
-      } else if constexpr (OP == POP_DEFECT || OP == POP_JACOBI) {
+      } else if constexpr (OP == POP_DEFECT || OP == POP_JACOBI || OP == POP_JACOBI_Z) {
         Row<EP, W> bb;
-        if constexpr (K::kBReg) bb = bcur[i];
+        if constexpr (K::kJZ) rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, bb);  // b centre
+        else if constexpr (K::kBReg) bb = bcur[i];
         else rload<EP, EP, W>(st + K::kXBytes + (tr + i) * K::kEpiRow + x0 * Bytes<EP>::v, bb);
         if constexpr (EP == P16) {
           const __half2 m1 = u2h(0xBC00BC00u);
@@ -595,7 +633,10 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
           } else {
             const Row<EP, W> dr = emul<EP, FTZ, W>(a.d16, r);  // vec_multiply(inv_diag, r)
             Row<EP, W> uc;
-            rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
+            if constexpr (K::kJZ) {
+              uc = bb;
+              jz_row<EP, FTZ, FMA, W>(a.d16, a.w16, uc);
+            } else rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
             Row<EP, W> un = efma<EP, FTZ, FMA, W>(a.w16, dr, uc);  // axpy(omega, t, u)
             if (x0 == 0) rzero_first<EP, W>(un);
             if (v) gstore<EP, W>(a.out, gi, un);
@@ -610,7 +651,10 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
           } else {
             const Row<EP, W> dr = emul<EP, FTZ, W>(dd, r);
             Row<EP, W> uc;
-            rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
+            if constexpr (K::kJZ) {
+              uc = bb;
+              jz_row<EP, FTZ, FMA, W>(dd, ww, uc);
+            } else rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
             Row<EP, W> un = efma<EP, FTZ, FMA, W>(ww, dr, uc);
             if (x0 == 0) rzero_first<EP, W>(un);
             if (v) gstore<EP, W>(a.out, gi, un);

@@ -3,6 +3,7 @@
 // compile in parallel.
 #pragma once
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "mpmg_internal.h"
@@ -12,17 +13,33 @@ namespace mpmg_impl {
 
 using namespace mpmg_dev;
 
-// CTA shape per (operand precision, compute precision, op, pitch)
-template <int LP, int CP, int OP, int P>
+// CTA shape per (operand precision, compute precision, op, pitch); V > 0
+// selects an alternative shape for tuning (MPMG_PLANE_VARIANT, binary16
+// Jacobi only)
+template <int LP, int CP, int OP, int P, int V = 0>
 struct PlaneCfg {
   static constexpr int W = P >= 256 ? 8 : P / 32;
   static constexpr int WX = P / (32 * W);
   static constexpr bool kWide = CP == P64 || (CP == P32 && LP != P16) || OP == POP_UPDATE;
   // output rows per thread and warp-rows per CTA
-  static constexpr int RY = kWide ? 2 : 4;
-  static constexpr int WY = WX >= 4 ? 1 : (WX == 2 ? 2 : 4);
-  static constexpr int NS = kWide && W == 8 ? 3 : 4;
+  static constexpr int RY0 = kWide ? 2 : 4;
+  static constexpr int WY0 = WX >= 4 ? 1 : (WX == 2 ? 2 : 4);
+  static constexpr int NS0 = kWide && W == 8 ? 3 : 4;
+  static constexpr int RY = V == 1 ? 2 : (V == 2 ? 2 : (V == 3 ? 4 : (V == 5 ? 1 : RY0)));
+  static constexpr int WY = V == 2 ? 8 : (V == 3 ? 2 : (V == 5 ? 8 : WY0));
+  static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : NS0);
+  static constexpr int OPT = V == 4 ? 1 : 0;
 };
+
+inline int plane_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_PLANE_VARIANT");
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 5) v = 0;
+  }
+  return v;
+}
 
 inline __half2 h2_of(double v) {
   const __half h = __double2half(v);
@@ -52,12 +69,12 @@ inline PlaneArgs plane_args(const mpmg_stencil& A, const mpmg_slab* slab = nullp
 // number of SMs of the current device (cached)
 int plane_num_sms();
 
-template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, int P>
+template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, int P, int V = 0>
 struct PlaneLaunch {
-  using C = PlaneCfg<LP, CP, OP, P>;
+  using C = PlaneCfg<LP, CP, OP, P, V>;
   static constexpr bool SKIPF = CP == P16;
-  using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS>;
-  static constexpr auto kernel = k_plane<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS>;
+  using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
+  static constexpr auto kernel = k_plane<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
 
   // grid: y-tiles x z-chunks, z-chunks sized so the grid is about one wave
   static dim3 grid(int* zc, int pz = P) {
@@ -122,11 +139,12 @@ inline bool faces_zero16(const mpmg_stencil& A) {
   return true;
 }
 
-// level op (DEFECT / JACOBI) through the plane kernels; false if not covered
+// level op (1 DEFECT / 2 JACOBI / 3 two JACOBI steps from zero, x = b) through
+// the plane kernels; false if not covered
 template <int LP>
 bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                     uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr) {
-  if (A.dim != 3 || (op != 1 && op != 2)) return false;
+  if (A.dim != 3 || (op != 1 && op != 2 && op != 3)) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
   if (LP == P16 && !faces_zero16(A)) return false;
   if (!aligned16(x) || !aligned16(b) || !aligned16(out)) return false;
@@ -139,8 +157,18 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
     constexpr int PP = decltype(pc)::value;
     if (op == 1) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_DEFECT, true, true, PP>::run(a, s)
                             : PlaneLaunch<LP, LP, LP, POP_DEFECT, false, true, PP>::run(a, s);
-    else *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP>::run(a, s)
-                    : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP>::run(a, s);
+    else if (op == 3) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, true, true, PP>::run(a, s)
+                                 : PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, false, true, PP>::run(a, s);
+    else if (LP == P16 && PP == 256 && !ftz && plane_variant() > 0) {
+      switch (plane_variant()) {
+        case 1: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 1>::run(a, s); break;
+        case 2: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 2>::run(a, s); break;
+        case 3: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 3>::run(a, s); break;
+        case 4: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 4>::run(a, s); break;
+        default: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 5>::run(a, s); break;
+      }
+    } else *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP>::run(a, s)
+                      : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP>::run(a, s);
   });
 }
 

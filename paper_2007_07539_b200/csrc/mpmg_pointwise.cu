@@ -75,28 +75,35 @@ __global__ void k_jacobi_zero(const void* __restrict__ bv, void* __restrict__ uv
   }
 }
 
-// transfer_product<P> single step (multigrid.cpp:166-195); weights exact
+// transfer_product<P> single step (multigrid.cpp:166-195). The weights are
+// 2^-k (k = number of straddled dimensions), built exactly in the compute
+// precision by exponent arithmetic -- no runtime conversion per product.
 template <int CP, bool FTZ, bool FMA> struct Xfer;
 template <bool FTZ, bool FMA> struct Xfer<P16, FTZ, FMA> {
   using T = __half;
   static __device__ __forceinline__ T zero() { return __ushort_as_half((unsigned short)0); }
-  static __device__ __forceinline__ T step(double w, T x, T acc) { return fma16s<FTZ, FMA>(__double2half(w), x, acc); }
+  static __device__ __forceinline__ T weight(int k) { return __ushort_as_half((unsigned short)(0x3C00 - (k << 10))); }
+  static __device__ __forceinline__ T step(T w, T x, T acc) { return fma16s<FTZ, FMA>(w, x, acc); }
   static __device__ __forceinline__ double wide(T v) { return (double)__half2float(v); }
 };
 template <bool FTZ, bool FMA> struct Xfer<P32, FTZ, FMA> {
   using T = float;
   static __device__ __forceinline__ T zero() { return 0.0f; }
+  static __device__ __forceinline__ T weight(int k) { return __int_as_float(0x3F800000 - (k << 23)); }
   // multigrid.cpp:178-184: the unfused form rounds the product to binary32
   // and flushes only the sum
-  static __device__ __forceinline__ T step(double w, T x, T acc) {
-    return f32<FTZ>(FMA ? __fmaf_rn((float)w, x, acc) : __fadd_rn(__fmul_rn((float)w, x), acc));
+  static __device__ __forceinline__ T step(T w, T x, T acc) {
+    return f32<FTZ>(FMA ? __fmaf_rn(w, x, acc) : __fadd_rn(__fmul_rn(w, x), acc));
   }
   static __device__ __forceinline__ double wide(T v) { return (double)v; }
 };
 template <bool FTZ, bool FMA> struct Xfer<P64, FTZ, FMA> {
   using T = double;
   static __device__ __forceinline__ T zero() { return 0.0; }
-  static __device__ __forceinline__ T step(double w, T x, T acc) { return fma64<FMA>(w, x, acc); }
+  static __device__ __forceinline__ T weight(int k) {
+    return __longlong_as_double(0x3FF0000000000000LL - ((long long)k << 52));
+  }
+  static __device__ __forceinline__ T step(T w, T x, T acc) { return fma64<FMA>(w, x, acc); }
   static __device__ __forceinline__ double wide(T v) { return v; }
 };
 
@@ -133,13 +140,17 @@ __global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_,
     for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
       for (int dx = -1; dx <= 1; ++dx) {
-        const double w = (dx == 0 ? 1.0 : 0.5) * (dy == 0 ? 1.0 : 0.5) * (dz == 0 ? 1.0 : 0.5);
-        acc = X::step(w, rf[cf + dz * pf + (long long)dy * Pf + dx], acc);
+        acc = X::step(X::weight((dx != 0) + (dy != 0) + (dz != 0)), rf[cf + dz * pf + (long long)dy * Pf + dx], acc);
       }
-  const double s = scale_dev ? *scale_dev : 1.0;
-  const double v = X::wide(acc) / s;
   const long long ci = (DIM == 3 ? (long long)cz * Pc * Pc : 0) + (long long)cy * Pc + cx;
-  static_cast<typename St<CPc>::T*>(rc_)[ci] = store_round<CPc, FTZ>(v);
+  if constexpr (FP == CPc) {
+    if (!scale_dev) {  // same precision, scale 1: the cast is the identity
+      static_cast<TF*>(rc_)[ci] = acc;
+      return;
+    }
+  }
+  const double s = scale_dev ? *scale_dev : 1.0;
+  static_cast<typename St<CPc>::T*>(rc_)[ci] = store_round<CPc, FTZ>(X::wide(acc) / s);
 }
 
 // prolongation + correction: one thread per fine interior node; parents per
@@ -156,17 +167,16 @@ __global__ void k_prolong(const void* __restrict__ cc_, void* __restrict__ uf_, 
   if (fx > Pf - 1 || fy > Pf - 1) return;
   const int Pc = Pf / 2;
   int px[2], py[2], pz[2];
-  double wx, wy, wz;
   const int nx = (fx & 1) ? 2 : 1, ny = (fy & 1) ? 2 : 1, nz = DIM == 3 ? ((fz & 1) ? 2 : 1) : 1;
-  px[0] = fx >> 1; px[1] = (fx + 1) >> 1; wx = (fx & 1) ? 0.5 : 1.0;
-  py[0] = fy >> 1; py[1] = (fy + 1) >> 1; wy = (fy & 1) ? 0.5 : 1.0;
-  pz[0] = fz >> 1; pz[1] = (fz + 1) >> 1; wz = DIM == 3 ? ((fz & 1) ? 0.5 : 1.0) : 1.0;
+  px[0] = fx >> 1; px[1] = (fx + 1) >> 1;
+  py[0] = fy >> 1; py[1] = (fy + 1) >> 1;
+  pz[0] = fz >> 1; pz[1] = (fz + 1) >> 1;
   TC acc = X::zero();
   for (int c = 0; c < nz; ++c)
     for (int b = 0; b < ny; ++b)
       for (int a = 0; a < nx; ++a) {
         const long long ci = (DIM == 3 ? (long long)pz[c] * Pc * Pc : 0) + (long long)py[b] * Pc + px[a];
-        acc = X::step(wx * wy * wz, cc[ci], acc);
+        acc = X::step(X::weight((fx & 1) + (fy & 1) + (DIM == 3 ? (fz & 1) : 0)), cc[ci], acc);
       }
   const double s = scale_dev ? *scale_dev : 1.0;
   const double v = X::wide(acc) * s;
@@ -319,7 +329,6 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
   const int ny = (fy & 1) ? 2 : 1, nz = DIM == 3 ? ((gz & 1) ? 2 : 1) : 1;
   const int py[2] = {fy >> 1, (fy + 1) >> 1};
   const int pz[2] = {(gz >> 1) - zc_lo + 1, ((gz + 1) >> 1) - zc_lo + 1};
-  const double wy = (fy & 1) ? 0.5 : 1.0, wz = DIM == 3 ? ((gz & 1) ? 0.5 : 1.0) : 1.0;
   // coarse values x0/2 .. x0/2+4 of each parent row
   TC c[2][2][5];
 #pragma unroll
@@ -333,6 +342,7 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
       }
     }
   const double s = scale_dev ? *scale_dev : 1.0;
+  const bool unit = !scale_dev;
   const long long fi = (DIM == 3 ? (long long)fz * Pf * Pf : 0) + (long long)fy * Pf + x0;
   V8<FP> u;
   u.load(uf_, fi);
@@ -341,7 +351,7 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
     const int fx = x0 + e;
     if (fx == 0) continue;  // ghost node stays zero
     const int nx = (fx & 1) ? 2 : 1;
-    const double wx = (fx & 1) ? 0.5 : 1.0;
+    const auto wk = X::weight((fx & 1) + (fy & 1) + (DIM == 3 ? (gz & 1) : 0));
     const int px0 = (fx >> 1) - x0 / 2;
     TC acc = X::zero();
 #pragma unroll
@@ -350,8 +360,10 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int a = 0; a < 2; ++a)
-          if (k < nz && j < ny && a < nx) acc = X::step(wx * wy * wz, c[k][j][px0 + a], acc);
-    const auto t = store_round<FP, FTZ>(X::wide(acc) * s);
+          if (k < nz && j < ny && a < nx) acc = X::step(wk, c[k][j][px0 + a], acc);
+    typename St<FP>::T t;
+    if constexpr (FP == CPc) t = unit ? acc : store_round<FP, FTZ>(X::wide(acc) * s);
+    else t = store_round<FP, FTZ>(X::wide(acc) * s);
     if constexpr (FP == P16) u.set(e, fma16s<FTZ, FMA>(__ushort_as_half((unsigned short)0x3C00), t, u.get(e)));
     else if constexpr (FP == P32) u.set(e, fma32<FTZ, FMA>(1.0f, t, u.get(e)));
     else u.set(e, fma64<FMA>(1.0, t, u.get(e)));

@@ -3,9 +3,9 @@
 // v_cycle, multigrid.cpp:282-393, and ir_solve, ir_solver.cpp:51-127),
 // re-designed for one B200:
 //   * every level vector lives in HBM in the ghost-aliased pitch layout;
-//   * a level with more than kClusterPoints unknowns runs the streaming
+//   * a level with more than kCoarsePoints unknowns runs the streaming
 //     stencil kernels; all coarser levels (and the CG base solve) run inside
-//     one thread-block-cluster kernel (mpmg_coarse.cu);
+//     one persistent cooperative kernel (mpmg_coarse.cu);
 //   * the outer loop runs on the device: a control kernel reduces ||r||,
 //     applies the reference's stopping rules and sets the condition of a CUDA
 //     graph WHILE node, so a whole solve is one graph launch with no host
@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -32,8 +33,14 @@ int set_cuda_error(cudaError_t e) {
 namespace {
 
 // levels with more interior unknowns than this run the streaming (plane)
-// kernels, one launch per operation; the rest run in the coarse cluster kernel
-constexpr long long kClusterPoints = 32768;
+// kernels, one launch per operation; the rest run inside the one persistent
+// cooperative coarse kernel (mpmg_coarse.cu)
+constexpr long long kCoarsePoints = 32768;
+// (MPMG_COARSE_POINTS / MPMG_CTA_POINTS override both thresholds for tuning)
+long long env_ll(const char* name, long long dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
 constexpr int kCtlThreads = 256;
 
 struct Level {
@@ -172,7 +179,13 @@ struct mpmg_solver {
     }
     cudaError_t e = cudaSuccess;
     void* cur = nullptr;
-    for (int k = 0; k < cfg.pre_steps && e == cudaSuccess; ++k) {
+    int k = 0;
+    if (cfg.pre_steps >= 2) {  // steps 1+2 from zero in one pass (result in u2, like the unfused pair)
+      e = launch_jacobi_zero2(L.A, L.b, L.u, L.u2, cfg.omega, L.omega_r, policy(), q);
+      cur = L.u2;
+      k = 2;
+    }
+    for (; k < cfg.pre_steps && e == cudaSuccess; ++k) {
       void* out = (cur == L.u) ? L.u2 : L.u;
       if (!cur) e = launch_jacobi_zero(L.A.dim, L.A.nodes, L.A.prec, L.b, out, L.omega_r, L.A.inv_diag, policy(), q);
       else e = launch_level_op(2, L.A, cur, L.b, out, cfg.omega, policy(), q);
@@ -418,7 +431,8 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
     L.omega_r = round_to(c.omega, prec, ftz);
     L.len = mpmg_padded_len(c.dim, nl);
     L.bytes = mpmg_bytes_per_value(prec);
-    L.big = (long long)mpmg_interior_len(c.dim, nl) > kClusterPoints && stencil_supported(c.dim, nl, prec);
+    L.big = (long long)mpmg_interior_len(c.dim, nl) > env_ll("MPMG_COARSE_POINTS", kCoarsePoints) &&
+            stencil_supported(c.dim, nl, prec);
   }
   // big levels must be a suffix (finest levels)
   for (int l = c.levels - 1; l >= 1; --l)
@@ -474,6 +488,10 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
     A.base_tol = c.base_tol;
     A.base_mode = c.base_mode;
     A.base_maxit = c.base_max_iterations;
+    A.cta_points = (int)env_ll("MPMG_CTA_POINTS", 4096);
+    A.debug = (int)env_ll("MPMG_COARSE_DEBUG", 0);
+    A.dbg = nullptr;
+    if (A.debug) e = S->alloc(&A.dbg, 64 * sizeof(long long));
     for (int l = 0; l < S->nc; ++l) {
       const Level& L = S->lv[l];
       CoarseLevel& C = A.lv[l];
@@ -539,8 +557,9 @@ int mpmg_solver_solve_device(mpmg_solver* S, const double* b_dev, double* u_dev,
   }
   if (e == cudaSuccess) e = cudaEventRecord(S->e0, q);
   bool graph_ok = false;
+  cudaError_t gerr = cudaSuccess;
   if (e == cudaSuccess && p.use_graph) {
-    if (!S->gvalid || !mpmg_solver::same_params(S->gkey, p)) S->build_graph(p);
+    if (!S->gvalid || !mpmg_solver::same_params(S->gkey, p)) gerr = S->build_graph(p);
     if (S->gvalid) {
       e = cudaGraphLaunch(S->exec, q);
       graph_ok = e == cudaSuccess;
@@ -577,6 +596,8 @@ int mpmg_solver_solve_device(mpmg_solver* S, const double* b_dev, double* u_dev,
     rep->final_residual = *S->final_h;
     rep->device_seconds = ms * 1e-3;
     rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rep->used_graph = graph_ok ? 1 : 0;
+    rep->graph_error = (int32_t)gerr;
   }
   if (st.diverged) {
     last_error() = "ir_solve: non-finite residual norm at iteration " + std::to_string(st.iterations);
@@ -668,6 +689,14 @@ int mpmg_solver_v_cycle(mpmg_solver* S, const double* b_host, double* c_host) {
   return finish(e);
 }
 
+int mpmg_solver_coarse_debug(mpmg_solver* S, long long* out, int32_t cap) {
+  if (!S || !out || cap < 1) return MPMG_EINVAL;
+  if (!S->cargs.dbg) return MPMG_EUNSUPPORTED;
+  cudaError_t e = cudaStreamSynchronize(S->s);
+  if (e == cudaSuccess) e = cudaMemcpy(out, S->cargs.dbg, (size_t)(cap < 64 ? cap : 64) * 8, cudaMemcpyDeviceToHost);
+  return finish(e);
+}
+
 int mpmg_solver_v_cycle_device(mpmg_solver* S, const void* b_dev, void* c_dev, void* stream) {
   if (!S || !b_dev || !c_dev) return MPMG_EINVAL;
   Level& F = S->lv.back();
@@ -722,7 +751,13 @@ int mpmg_solver_level_op(mpmg_solver* S, int op, int l, const double* in0, const
       e = upload_values(S, dim, nodes, prec, in1, L.b);
       void* cur = nullptr;
       if (e == cudaSuccess && in0) { e = upload_values(S, dim, nodes, prec, in0, L.u); cur = L.u; }
-      for (int k = 0; k < steps && e == cudaSuccess; ++k) {
+      int k = 0;
+      if (e == cudaSuccess && !in0 && steps >= 2) {  // the fused first two steps (as in the V-cycle)
+        e = launch_jacobi_zero2(L.A, L.b, L.u, L.u2, S->cfg.omega, L.omega_r, S->policy(), q);
+        cur = L.u2;
+        k = 2;
+      }
+      for (; k < steps && e == cudaSuccess; ++k) {
         void* o = (cur == L.u) ? L.u2 : L.u;
         if (!cur) e = launch_jacobi_zero(dim, nodes, prec, L.b, o, L.omega_r, L.A.inv_diag, S->policy(), q);
         else e = launch_level_op(2, L.A, cur, L.b, o, S->cfg.omega, S->policy(), q);

@@ -229,7 +229,11 @@ class CudaOps:
         return C.byref(SlabC(s.nz, s.z_lo, s.halo_lo, s.halo_hi))
 
     def _stream(self):
-        return self.torch.cuda.current_stream().cuda_stream
+        # torch's default stream is the legacy NULL stream (handle 0); pass
+        # cudaStreamLegacy explicitly -- NULL means "the solver's own stream"
+        # to the mpmg_solver_* entry points
+        s = self.torch.cuda.current_stream().cuda_stream
+        return s if s else 1
 
     def _ok(self, rc, what):
         if rc != 0:

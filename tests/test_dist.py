@@ -196,7 +196,85 @@ def test_gpu_slabs_match_single_gpu(variant):
     assert np.array_equal(c1, c2)
     for res, plan in ((one, p1), (two, p2)):
         u = compact_of_slabs([t[2] for t in res], plan, torch)
-        assert res[0][5], "not converged"
+        assert res[0][5], f"not converged: its {res[0][3]} hist {res[0][4][:6]} ... {res[0][4][-3:]} ref {rep.residual_history[:4]}"
         assert abs(res[0][3] - rep.iterations) <= 1
         assert np.linalg.norm(u - u_ref) <= 1e-9 * np.linalg.norm(u_ref)
         assert res[0][6] < tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["h_mg", "d_mg"])
+def test_gpu_slab_ops_match_whole_level(variant):
+    """Each sm_100a slab kernel on two slabs (halos copied by hand, one
+    process) equals the same kernel on the whole level, value for value."""
+    import paper_2007_07539_b200 as mg
+    from paper_2007_07539_b200.dist import CudaOps
+    nodes, levels = 129, 7
+    p1, p2 = SlabPlan(nodes, levels, 1), SlabPlan(nodes, levels, 2)
+    o1, o2 = CudaOps(p1, variant, ftz=False), CudaOps(p2, variant, ftz=False)
+    F = levels - 1
+    P = p1.P[F]
+    pl = P * P
+    rng = np.random.default_rng(3)
+    dt = o1.dt[o1.prec[F]]
+
+    def whole(vals):
+        t = torch.zeros(p1.slab_len(F, 0), dtype=torch.float64)
+        v = t[: P * pl].view(P, P, P)
+        v[1:P, 1:P, 1:P] = torch.from_numpy(vals.reshape(P - 1, P - 1, P - 1))
+        return t
+
+    def split(t_whole, plan, l):
+        Pl = plan.P[l]
+        out = []
+        for r in range(2):
+            s = plan.slab(l, r)
+            loc = torch.zeros(plan.slab_len(l, r), dtype=t_whole.dtype, device=t_whole.device)
+            loc[: (s.nz + 2) * Pl * Pl] = t_whole[(s.z_lo - 1) * Pl * Pl:(s.z_lo + s.nz + 1) * Pl * Pl]
+            out.append(loc)
+        return out
+
+    def owned(parts, plan, l):
+        Pl = plan.P[l]
+        res = []
+        for r, t in enumerate(parts):
+            s = plan.slab(l, r)
+            res.append(t[Pl * Pl:(1 + s.nz) * Pl * Pl].double().cpu())
+        return torch.cat(res)
+
+    vals = rng.uniform(-1, 1, (P - 1) ** 3) * 1e-2
+    u = whole(vals).to(dt).cuda()
+    b = whole(rng.uniform(-1, 1, (P - 1) ** 3)).to(dt).cuda()
+    s1 = p1.slab(F, 0)
+    out1 = torch.zeros_like(u)
+    o1.jacobi(F, s1, b, u, out1)
+    us, bs = split(u, p2, F), split(b, p2, F)
+    outs = [torch.zeros_like(x) for x in us]
+    for r in range(2):
+        o2.jacobi(F, p2.slab(F, r), bs[r], us[r], outs[r])
+    torch.cuda.synchronize()
+    ref = out1[pl:P * pl].double().cpu()
+    assert torch.equal(owned(outs, p2, F), ref), "slab jacobi"
+    # defect + restriction (the fine lower halo comes from the whole array)
+    r1 = torch.zeros_like(u)
+    o1.defect(F, s1, b, u, r1)
+    rs = [torch.zeros_like(x) for x in us]
+    for r in range(2):
+        o2.defect(F, p2.slab(F, r), bs[r], us[r], rs[r])
+    assert torch.equal(owned(rs, p2, F), r1[pl:P * pl].double().cpu()), "slab defect"
+    rsplit = split(r1, p2, F)
+    Pc = p1.P[F - 1]
+    c1 = torch.zeros(p1.slab_len(F - 1, 0), dtype=o1.dt[o1.prec[F - 1]], device="cuda")
+    o1.restrict(F, s1, p1.slab(F - 1, 0), r1, c1)
+    cs = [torch.zeros(p2.slab_len(F - 1, r), dtype=c1.dtype, device="cuda") for r in range(2)]
+    for r in range(2):
+        o2.restrict(F, p2.slab(F, r), p2.slab(F - 1, r), rsplit[r], cs[r])
+    assert torch.equal(owned(cs, p2, F - 1), c1[Pc * Pc:Pc * Pc * Pc].double().cpu()), "slab restrict"
+    # prolongation (coarse upper halo from the whole array)
+    csplit = split(c1, p2, F - 1)
+    u1 = u.clone()
+    o1.prolong(F, s1, p1.slab(F - 1, 0), c1, u1)
+    u2 = [x.clone() for x in us]
+    for r in range(2):
+        o2.prolong(F, p2.slab(F, r), p2.slab(F - 1, r), csplit[r], u2[r])
+    assert torch.equal(owned(u2, p2, F), u1[pl:P * pl].double().cpu()), "slab prolong"
