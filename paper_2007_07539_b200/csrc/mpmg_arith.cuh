@@ -19,6 +19,15 @@ namespace mpmg_dev {
 
 enum { P16 = 0, P32 = 1, P64 = 2 };
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor
+// drains; pdl_wait() blocks until the predecessor grid has completed and its
+// writes are visible, so it must precede every read of predecessor output.
+// pdl_launch() lets the successor grid be scheduled early. Both are no-ops
+// for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 

@@ -318,11 +318,19 @@ struct Coarse {
     else return (double)v;
   }
 
-  // CG on level 0 (multigrid.cpp:91-151), CTA 0 only
+  // CG on level 0 (multigrid.cpp:91-151), CTA 0 only; a base level of <= 32
+  // unknowns (every max-depth hierarchy) runs on warp 0 alone with warp
+  // barriers and shuffles instead of CTA-wide barriers
   template <int PR>
   __device__ void cg(const CoarseLevel& L, const void* bv, void* uv) {
+    if (points(L).n <= 32) cg_impl<PR, true>(L, bv, uv);
+    else cg_impl<PR, false>(L, bv, uv);
+  }
+  template <int PR, bool WARP>
+  __device__ void cg_impl(const CoarseLevel& L, const void* bv, void* uv) {
     using OP = O<PR>;
     using T = typename OP::T;
+    if (WARP && threadIdx.x >= 32) return;
     __shared__ double sh;
     const T* b = static_cast<const T*>(bv);
     T* u = static_cast<T*>(uv);
@@ -333,16 +341,24 @@ struct Coarse {
     T* best = static_cast<T*>(cgp[4]);
     const Pt pt = points(L);
     auto dot = [&](const T* x, const T* y) -> double {
-      __syncthreads();
-      if (threadIdx.x == 0) sh = dot_seq(pt, x, y);
-      __syncthreads();
-      const double v = sh;
-      __syncthreads();
-      return v;
+      if constexpr (WARP) {
+        __syncwarp();
+        double v = 0.0;
+        if (threadIdx.x == 0) v = dot_seq(pt, x, y);
+        return __shfl_sync(0xffffffffu, v, 0);
+      } else {
+        __syncthreads();
+        if (threadIdx.x == 0) sh = dot_seq(pt, x, y);
+        __syncthreads();
+        const double v = sh;
+        __syncthreads();
+        return v;
+      }
     };
     auto each = [&](auto&& f) {
-      for (int k = threadIdx.x; k < pt.n; k += blockDim.x) f(pt.idx(k));
-      __syncthreads();
+      for (int k = threadIdx.x; k < pt.n; k += (WARP ? 32 : (int)blockDim.x)) f(pt.idx(k));
+      if constexpr (WARP) __syncwarp();
+      else __syncthreads();
     };
     const int max_it = a.base_maxit > 0 ? a.base_maxit : 10 * pt.n;
     each([&](int i) {

@@ -6,12 +6,32 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "mpmg_gpu.h"
 
 namespace mpmg_impl {
 
 inline int pitch(int nodes) { return nodes - 1; }
+
+// launch with programmatic dependent launch enabled (MPMG_PDL=0 disables);
+// the kernel must call mpmg_dev::pdl_wait() before reading predecessor data
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // binary16 RNE rounding with optional flush-after-rounding, in the binary64
 // value domain (same contract as the reference's quantize_fp16,

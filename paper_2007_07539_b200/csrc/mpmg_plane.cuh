@@ -466,7 +466,6 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   unsigned char* stages = smem + 128;
 
-  if (a.gate && *a.gate == 0) return;  // uniform across the grid
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wx = warp % WX, wy = warp / WX;
@@ -508,6 +507,9 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();    // predecessor output visible from here on
+  pdl_launch();  // let the next kernel's CTAs be scheduled as ours retire
+  if (a.gate && *a.gate == 0) return;  // uniform across the grid
   if (tid == 0) {
     for (int k = 0; k < NS - 1 && k < NQ; ++k) issue(k);
   }

@@ -104,8 +104,7 @@ struct PlaneLaunch {
     const dim3 g = grid(&zc, a.pz);
     a.zc = zc;
     a.ty = K::TY;
-    kernel<<<g, K::kThreads, K::kSmem, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(kernel, g, dim3(K::kThreads), K::kSmem, s, a);
   }
 
   static int partials(int pz = P) {

@@ -59,6 +59,8 @@ __global__ void k_pack(const T* __restrict__ src, T* __restrict__ dst, long long
 template <int PREC, bool FTZ, bool FMA>
 __global__ void k_jacobi_zero(const void* __restrict__ bv, void* __restrict__ uv, long long len, double w,
                               double d) {
+  pdl_wait();
+  pdl_launch();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= len) return;
   if constexpr (PREC == P16) {
@@ -121,6 +123,8 @@ template <> __device__ __forceinline__ double store_round<P64, false>(double v) 
 template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
 __global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_, int Pc, const double* scale_dev,
                            int zoff = 0) {
+  pdl_wait();
+  pdl_launch();
   using X = Xfer<FP, FTZ, FMA>;
   using TF = typename X::T;
   const TF* rf = static_cast<const TF*>(rf_);
@@ -158,6 +162,8 @@ __global__ void k_restrict(const void* __restrict__ rf_, void* __restrict__ rc_,
 // outermost (mesh_fem.cpp:222-252). Boundary parents read the stored zeros.
 template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
 __global__ void k_prolong(const void* __restrict__ cc_, void* __restrict__ uf_, int Pf, const double* scale_dev) {
+  pdl_wait();
+  pdl_launch();
   using X = Xfer<CPc, FTZ, FMA>;
   using TC = typename X::T;
   const TC* cc = static_cast<const TC*>(cc_);
@@ -193,6 +199,8 @@ __global__ void k_prolong(const void* __restrict__ cc_, void* __restrict__ uf_, 
 template <int PREC, bool FTZ>
 __global__ void k_downcast(const double* __restrict__ x, void* __restrict__ out, long long len,
                            const double* alpha, int scale_enabled) {
+  pdl_wait();
+  pdl_launch();
   const double a = *alpha;
   const double s = (scale_enabled && a > 0.0) ? a : 1.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
@@ -262,6 +270,8 @@ __device__ __forceinline__ double div_by(double x, double s, double y) {
 template <int PREC, bool FTZ>
 __global__ void k_downcast8(const double* __restrict__ x, void* __restrict__ out, long long len,
                             const double* alpha, int scale_enabled) {
+  pdl_wait();
+  pdl_launch();
   const double a = *alpha;
   const double s = (scale_enabled && a > 0.0) ? a : 1.0;
   const double y = __drcp_rn(s);
@@ -294,6 +304,8 @@ __device__ __forceinline__ typename St<PREC>::T jz_one(typename St<PREC>::T b, d
 
 template <int PREC, bool FTZ, bool FMA>
 __global__ void k_jacobi_zero8(const void* __restrict__ bv, void* __restrict__ uv, long long len, double w, double d) {
+  pdl_wait();
+  pdl_launch();
   const long long n8 = len / 8;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n8; g += (long long)gridDim.x * blockDim.x) {
     V8<PREC> b;
@@ -315,6 +327,8 @@ __global__ void k_jacobi_zero8(const void* __restrict__ bv, void* __restrict__ u
 template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
 __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_, int Pf, const double* scale_dev,
                            int zf_lo = 1, int zc_lo = 1) {
+  pdl_wait();
+  pdl_launch();
   using X = Xfer<CPc, FTZ, FMA>;
   using TC = typename X::T;
   const TC* cc = static_cast<const TC*>(cc_);
@@ -346,6 +360,33 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
   const long long fi = (DIM == 3 ? (long long)fz * Pf * Pf : 0) + (long long)fy * Pf + x0;
   V8<FP> u;
   u.load(uf_, fi);
+  if constexpr (FP == P16 && CPc == P16) {
+    if (unit) {
+      // binary16, unit scale: fine pairs (2j, 2j+1) in one half2. Per parent
+      // row the even node takes w c_j, the odd one (w/2) c_j then (w/2)
+      // c_{j+1} -- the same per-node order as below; the even lane's extra
+      // fma(0, c, acc) leaves acc unchanged (up to the sign of a zero)
+      const int kyz = (fy & 1) + (DIM == 3 ? (gz & 1) : 0);
+      const __half2 w1 = __halves2half2(X::weight(kyz), X::weight(kyz + 1));
+      const __half2 w2 = __halves2half2(__ushort_as_half((unsigned short)0), X::weight(kyz + 1));
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        __half2 acc = u2h(0u);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (k < nz && j < ny) {
+              acc = fma16<FTZ, FMA>(w1, __half2half2(c[k][j][p]), acc);
+              acc = fma16<FTZ, FMA>(w2, __half2half2(c[k][j][p + 1]), acc);
+            }
+        u.h[p] = fma16<FTZ, FMA>(u2h(0x3C003C00u), acc, u.h[p]);  // axpy(1, t, u)
+      }
+      if (x0 == 0) u.set(0, __ushort_as_half((unsigned short)0));  // ghost node
+      u.store(uf_, fi);
+      return;
+    }
+  }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int fx = x0 + e;
@@ -369,6 +410,53 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
     else u.set(e, fma64<FMA>(1.0, t, u.get(e)));
   }
   u.store(uf_, fi);
+}
+
+// restriction, 4 consecutive coarse x per thread (Pc % 4 == 0, no scale,
+// same precision on both levels): each fine row segment 8g-1 .. 8g+7 is one
+// aligned 8-value vector load plus one scalar, shared by the 4 outputs;
+// per-output slot order (dz, dy, dx) as k_restrict. zoff as in k_restrict.
+template <int DIM, int FP, bool FTZ, bool FMA>
+__global__ void k_restrict4(const void* __restrict__ rf_, void* __restrict__ rc_, int Pc, int zoff, int nzc) {
+  pdl_wait();
+  pdl_launch();
+  using X = Xfer<FP, FTZ, FMA>;
+  using T = typename X::T;
+  const int groups = Pc / 4;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per_plane = (long long)groups * (Pc - 1);
+  if (tid >= per_plane * (DIM == 3 ? nzc : 1)) return;
+  const int cz = DIM == 3 ? (int)(tid / per_plane) + 1 : 0;
+  const int rem = (int)(tid % per_plane);
+  const int cy = rem / groups + 1;
+  const int g = rem % groups;
+  const int Pf = 2 * Pc;
+  const long long pf = (long long)Pf * Pf;
+  const T* rf = static_cast<const T*>(rf_);
+  T acc[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) acc[o] = X::zero();
+#pragma unroll
+  for (int dz = (DIM == 3 ? -1 : 0); dz <= (DIM == 3 ? 1 : 0); ++dz)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const long long row = (DIM == 3 ? (long long)(2 * cz + zoff + dz) * pf : 0) + (long long)(2 * cy + dy) * Pf;
+      V8<FP> v;
+      v.load(rf, row + 8 * g);
+      const T left = g > 0 ? rf[row + 8 * g - 1] : X::zero();
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int e = 2 * o + dx;  // fine offset within the segment
+          const T x = e < 0 ? left : v.get(e);
+          acc[o] = X::step(X::weight((dx != 0) + (dy != 0) + (dz != 0)), x, acc[o]);
+        }
+    }
+  if (g == 0) acc[0] = X::zero();  // cx = 0 is the boundary ghost
+  T* rc = static_cast<T*>(rc_) + (DIM == 3 ? (long long)cz * Pc * Pc : 0) + (long long)cy * Pc + 4 * g;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) rc[o] = acc[o];
 }
 
 // deterministic per-block partial sums of x_i^2 (fixed grid, fixed order)
@@ -462,11 +550,12 @@ cudaError_t launch_jacobi_zero_len(size_t len, int prec, const void* b, void* u,
     return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
       constexpr int PR = decltype(pc)::value;
       constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
+      cudaError_t e;
       if (vec)
-        k_jacobi_zero8<PR, T, M><<<grid8(len), kThreads, 0, s>>>(b, u, (long long)len, omega_r, invdiag_r);
+        e = launch_pdl(k_jacobi_zero8<PR, T, M>, dim3(grid8(len)), dim3(kThreads), 0, s, b, u, (long long)len, omega_r, invdiag_r);
       else
-        k_jacobi_zero<PR, T, M><<<blocks_for(len), kThreads, 0, s>>>(b, u, (long long)len, omega_r, invdiag_r);
-      return cudaGetLastError();
+        e = launch_pdl(k_jacobi_zero<PR, T, M>, dim3(blocks_for(len)), dim3(kThreads), 0, s, b, u, (long long)len, omega_r, invdiag_r);
+      return e;
     });
   });
 }
@@ -477,14 +566,25 @@ cudaError_t launch_restrict(int dim, int fine_nodes, int fine_prec, int coarse_p
   if (Pc < 2) return cudaSuccess;
   const dim3 block(32, 8);
   const dim3 grid((Pc - 1 + 31) / 32, (Pc - 1 + 7) / 8, dim == 3 ? Pc - 1 : 1);
+  if (!scale_dev && fine_prec == coarse_prec && Pc % 4 == 0 && Pc >= 8 && aligned64(r_fine)) {
+    const long long n = (long long)(Pc / 4) * (Pc - 1) * (dim == 3 ? Pc - 1 : 1);
+    const unsigned blocks = (unsigned)((n + kThreads - 1) / kThreads);
+    return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
+      return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+        constexpr int F = decltype(fp)::value;
+        constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
+        if (dim == 3) return launch_pdl(k_restrict4<3, F, T, M>, dim3(blocks), dim3(kThreads), 0, s, r_fine, r_coarse, Pc, 0, Pc - 1);
+        return launch_pdl(k_restrict4<2, F, T, M>, dim3(blocks), dim3(kThreads), 0, s, r_fine, r_coarse, Pc, 0, 1);
+      });
+    });
+  }
   return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
     return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
       return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
         constexpr int F = decltype(fp)::value, Cc = decltype(cp)::value;
         constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
-        if (dim == 3) k_restrict<3, F, Cc, T, M><<<grid, block, 0, s>>>(r_fine, r_coarse, Pc, scale_dev);
-        else k_restrict<2, F, Cc, T, M><<<grid, block, 0, s>>>(r_fine, r_coarse, Pc, scale_dev);
-        return cudaGetLastError();
+        if (dim == 3) return launch_pdl(k_restrict<3, F, Cc, T, M>, grid, block, 0, s, r_fine, r_coarse, Pc, scale_dev, 0);
+        return launch_pdl(k_restrict<2, F, Cc, T, M>, grid, block, 0, s, r_fine, r_coarse, Pc, scale_dev, 0);
       });
     });
   });
@@ -503,11 +603,11 @@ cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_pr
         constexpr int F = decltype(fp)::value, Cc = decltype(cp)::value;
         constexpr bool T = decltype(ft)::value, M = decltype(fm)::value;
         if (vec) {
-          if (dim == 3) k_prolong8<3, F, Cc, T, M><<<grid8v, kThreads, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
-          else k_prolong8<2, F, Cc, T, M><<<grid8v, kThreads, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
-        } else if (dim == 3) k_prolong<3, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
-        else k_prolong<2, F, Cc, T, M><<<grid, block, 0, s>>>(c_coarse, u_fine, Pf, scale_dev);
-        return cudaGetLastError();
+          if (dim == 3) return launch_pdl(k_prolong8<3, F, Cc, T, M>, grid8v, dim3(kThreads), 0, s, c_coarse, u_fine, Pf, scale_dev, 1, 1);
+          return launch_pdl(k_prolong8<2, F, Cc, T, M>, grid8v, dim3(kThreads), 0, s, c_coarse, u_fine, Pf, scale_dev, 1, 1);
+        }
+        if (dim == 3) return launch_pdl(k_prolong<3, F, Cc, T, M>, grid, block, 0, s, c_coarse, u_fine, Pf, scale_dev);
+        return launch_pdl(k_prolong<2, F, Cc, T, M>, grid, block, 0, s, c_coarse, u_fine, Pf, scale_dev);
       });
     });
   });
@@ -524,6 +624,16 @@ cudaError_t launch_restrict_slab(int fine_nodes, const mpmg_slab& sf, const mpmg
   const dim3 block(32, 8);
   const dim3 grid((Pc - 1 + 31) / 32, (Pc - 1 + 7) / 8, sc.nz);
   const int zoff = 2 * sc.z_lo - sf.z_lo - 1;
+  if (fine_prec == coarse_prec && Pc % 4 == 0 && Pc >= 8 && aligned64(r_fine)) {
+    const long long n = (long long)(Pc / 4) * (Pc - 1) * sc.nz;
+    return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
+      return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
+        k_restrict4<3, decltype(fp)::value, decltype(ft)::value, decltype(fm)::value>
+            <<<(unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(r_fine, r_coarse, Pc, zoff, sc.nz);
+        return cudaGetLastError();
+      });
+    });
+  }
   return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
     return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
       return with_ftz_fma(policy, [&](auto ft, auto fm) -> cudaError_t {
@@ -563,12 +673,10 @@ cudaError_t launch_downcast_len(size_t len, const double* x, void* out, int prec
   if (aligned64(x) && aligned64(out))
     return with_prec(prec, [&](auto pc) -> cudaError_t {
       if (policy & MPMG_FTZ)
-        k_downcast8<decltype(pc)::value, true><<<grid8(len), kThreads, 0, s>>>(x, out, (long long)len, alpha_dev,
-                                                                              scale_enabled);
-      else
-        k_downcast8<decltype(pc)::value, false><<<grid8(len), kThreads, 0, s>>>(x, out, (long long)len, alpha_dev,
-                                                                               scale_enabled);
-      return cudaGetLastError();
+        return launch_pdl(k_downcast8<decltype(pc)::value, true>, dim3(grid8(len)), dim3(kThreads), 0, s, x, out,
+                          (long long)len, alpha_dev, scale_enabled);
+      return launch_pdl(k_downcast8<decltype(pc)::value, false>, dim3(grid8(len)), dim3(kThreads), 0, s, x, out,
+                        (long long)len, alpha_dev, scale_enabled);
     });
   return with_prec(prec, [&](auto pc) -> cudaError_t {
     if (policy & MPMG_FTZ)

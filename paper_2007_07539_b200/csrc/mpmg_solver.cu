@@ -24,6 +24,15 @@
 namespace mpmg_impl {
 
 thread_local std::string g_err;
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_PDL");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
 std::string& last_error() { return g_err; }
 int set_cuda_error(cudaError_t e) {
   g_err = cudaGetErrorString(e);
@@ -59,6 +68,7 @@ struct Level {
 __global__ void k_control(IrState* st, const double* p_main, int n_main, const double* p_ref, int n_ref,
                           double* hist, int hist_cap, double tol, int max_it, int scale_enabled, int refresh,
                           int increment, cudaGraphConditionalHandle cond, int use_cond) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // pdl_wait (mpmg_arith.cuh)
   __shared__ double red[kCtlThreads];
   const bool ref = increment && st->refresh_now;
   const double* p = ref ? p_ref : p_main;
@@ -265,10 +275,9 @@ struct mpmg_solver {
     if (e == cudaSuccess && p.residual_refresh_interval > 0)  // ir_solver.cpp:115-119 (gated on device)
       e = launch_defect64(A64, b, u, r, partD, fma(), false, q, &st->refresh_now);
     if (e == cudaSuccess) {
-      k_control<<<1, kCtlThreads, 0, q>>>(st, partU, nU, partD, nD, hist, hist_cap, p.outer_tolerance,
-                                            p.max_outer_iterations, scale_enabled(p),
-                                            p.residual_refresh_interval, 1, h, use_cond);
-      e = cudaGetLastError();
+      e = launch_pdl(k_control, dim3(1), dim3(kCtlThreads), 0, q, st, (const double*)partU, nU,
+                     (const double*)partD, nD, hist, hist_cap, p.outer_tolerance, p.max_outer_iterations,
+                     scale_enabled(p), p.residual_refresh_interval, 1, h, use_cond);
     }
     return e;
   }
