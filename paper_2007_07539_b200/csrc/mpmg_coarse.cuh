@@ -27,6 +27,7 @@
 #include "mpmg_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mpmg_impl {
 
@@ -35,6 +36,8 @@ using namespace mpmg_dev;
 namespace coarse_detail {
 
 constexpr int kThreads = 512;
+// top levels up to this many unknowns run on one 16-CTA cluster
+constexpr long long kClusterPoints = 65536;
 constexpr int kCtaPoints = 4096;
 
 template <int PR> struct T_;
@@ -98,10 +101,10 @@ struct Lv {
     }
     return k;
   }
-  // A x at padded index i (all 3^dim taps in slot order; ghosts are zero)
-  template <int DIM>
-  static __device__ __forceinline__ T apply_d(const Taps& k, const T* x, int i, int P) {
-    const int pl = DIM == 3 ? P * P : 0;
+  // A x at one point (all 3^dim taps in slot order; ghosts are zero);
+  // ld(dz, dy, dx) returns the neighbour value
+  template <int DIM, typename LD>
+  static __device__ __forceinline__ T apply_f(const Taps& k, LD&& ld) {
     if constexpr (PR == P16 && ACC32) {  // Fp16Accum::FP32 (kernels.cpp:151-162)
       float acc = 0.0f;
       int t = 0;
@@ -110,8 +113,7 @@ struct Lv {
 #pragma unroll
         for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-          for (int dx = -1; dx <= 1; ++dx, ++t)
-            acc = fma32<FTZ, FMA>(k.f[t], __half2float(ldcg(x + i + dz * pl + dy * P + dx)), acc);
+          for (int dx = -1; dx <= 1; ++dx, ++t) acc = fma32<FTZ, FMA>(k.f[t], __half2float(ld(dz, dy, dx)), acc);
       return f16s<FTZ>(__float2half_rn(acc));
     } else {
       T acc = zero();
@@ -121,12 +123,23 @@ struct Lv {
 #pragma unroll
         for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-          for (int dx = -1; dx <= 1; ++dx, ++t) acc = fma(k.t[t], ldcg(x + i + dz * pl + dy * P + dx), acc);
+          for (int dx = -1; dx <= 1; ++dx, ++t) acc = fma(k.t[t], ld(dz, dy, dx), acc);
       return acc;
     }
   }
+  template <int DIM>
+  static __device__ __forceinline__ T apply_d(const Taps& k, const T* x, int i, int P) {
+    const int pl = DIM == 3 ? P * P : 0;
+    return apply_f<DIM>(k, [&](int dz, int dy, int dx) { return ldcg(x + i + dz * pl + dy * P + dx); });
+  }
   static __device__ __forceinline__ T apply(const Taps& k, int dim, const T* x, int i, int P) {
     return dim == 3 ? apply_d<3>(k, x, i, P) : apply_d<2>(k, x, i, P);
+  }
+  // A x on a one-unknown level: every neighbour is a (zero) ghost. The same
+  // operation sequence as apply(), on a register value.
+  static __device__ __forceinline__ T apply1(const Taps& k, int dim, T x) {
+    auto ld = [&](int dz, int dy, int dx) { return (dz | dy | dx) == 0 ? x : zero(); };
+    return dim == 3 ? apply_f<3>(k, ld) : apply_f<2>(k, ld);
   }
 };
 
@@ -153,6 +166,11 @@ __device__ __forceinline__ Pt points(const CoarseLevel& L) {
 }
 
 __device__ __forceinline__ void grid_sync() { cooperative_groups::this_grid().sync(); }
+// all CTAs of the (single-cluster) grid: the hardware cluster barrier, with
+// release/acquire at cluster scope ordering the global-memory level data
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
 
 // UP: the one precision of every level (P16/P32/P64: H_MG, D_MG -- a single
 // code path, a third of the instruction footprint), or 3 for mixed cascades
@@ -164,9 +182,14 @@ struct Coarse {
   void* const* cgp;  // CG scratch r, p, ap, s, best
   const __half (*t16)[27];
   const float (*t32)[27];
+  const bool clustered;  // the grid is one thread-block cluster (else a cooperative grid)
   __device__ Coarse(const CoarseArgs& args, CoarseLevel* table, void* const* cg, const __half (*a16)[27],
-                    const float (*a32)[27])
-      : a(args), rank(blockIdx.x), ncta(gridDim.x), lv(table), cgp(cg), t16(a16), t32(a32) {}
+                    const float (*a32)[27], bool cluster)
+      : a(args), rank(blockIdx.x), ncta(gridDim.x), lv(table), cgp(cg), t16(a16), t32(a32), clustered(cluster) {}
+  __device__ void gsync() {
+    if (clustered) cluster_sync();
+    else grid_sync();
+  }
   template <int PR>
   __device__ typename Lv<PR, FTZ, FMA, ACC32>::Taps taps_of(const CoarseLevel& L) const {
     const int l = (int)(&L - lv);
@@ -191,7 +214,7 @@ struct Coarse {
   __device__ bool in_team(const CoarseLevel& L) const { return !small(L) || rank == 0; }
   __device__ void sync(const CoarseLevel& L) {
     if (small(L)) __syncthreads();
-    else grid_sync();
+    else gsync();
   }
 
   template <typename F>
@@ -323,8 +346,60 @@ struct Coarse {
   // barriers and shuffles instead of CTA-wide barriers
   template <int PR>
   __device__ void cg(const CoarseLevel& L, const void* bv, void* uv) {
-    if (points(L).n <= 32) cg_impl<PR, true>(L, bv, uv);
+    if (points(L).n == 1) cg_one<PR>(L, bv, uv);
+    else if (points(L).n <= 32) cg_impl<PR, true>(L, bv, uv);
     else cg_impl<PR, false>(L, bv, uv);
+  }
+  // cg_impl on a one-unknown base level (every max-depth hierarchy): the
+  // identical operation sequence, every vector a register of thread 0, so an
+  // iteration is a short dependent chain instead of barriers and shared
+  // memory round trips (an FP16 base level runs all 10 iterations)
+  template <int PR>
+  __device__ void cg_one(const CoarseLevel& L, const void* bv, void* uv) {
+    using OP = O<PR>;
+    using T = typename OP::T;
+    if (threadIdx.x != 0) return;
+    const Pt pt = points(L);
+    const int i0 = pt.idx(0);
+    const T b = ldcg(static_cast<const T*>(bv) + i0);
+    T* uo = static_cast<T*>(uv) + i0;
+    const double bw = wide_v(b);
+    const double norm_b = sqrt(__fma_rn(bw, bw, 0.0));
+    T u = OP::zero(), r = b, p = b, best = OP::zero();
+    if (norm_b == 0.0) {
+      *uo = u;
+      return;
+    }
+    const int max_it = a.base_maxit > 0 ? a.base_maxit : 10;
+    const double thr = a.base_mode == 0 ? a.base_tol * norm_b : a.base_tol;
+    double rz = __fma_rn(wide_v(r), wide_v(r), 0.0);
+    double true_res = norm_b, best_res = norm_b;
+    int it = 0;
+    const T m1 = OP::from(-1.0);
+    const auto tk = taps_of<PR>(L);
+    while (true_res >= thr && it < max_it) {
+      const T ap = OP::apply1(tk, L.dim, p);
+      const double pAp = __fma_rn(wide_v(p), wide_v(ap), 0.0);
+      if (!(pAp > 0.0) || !isfinite(pAp)) break;
+      const double alpha = rz / pAp;
+      const T al = OP::from(alpha), mal = OP::from(-alpha);
+      u = OP::fma(al, p, u);
+      r = OP::fma(mal, ap, r);
+      const double rz_new = __fma_rn(wide_v(r), wide_v(r), 0.0);
+      ++it;
+      const T sc = OP::fma(m1, OP::apply1(tk, L.dim, u), b);
+      true_res = sqrt(__fma_rn(wide_v(sc), wide_v(sc), 0.0));
+      if (true_res < best_res) {
+        best_res = true_res;
+        best = u;
+      }
+      if (rz == 0.0) break;
+      const T be = OP::from(rz_new / rz);
+      p = OP::fma(be, p, r);
+      rz = rz_new;
+    }
+    *uo = true_res > best_res ? best : u;
+    if (a.cg_iterations) *a.cg_iterations = it;
   }
   template <int PR, bool WARP>
   __device__ void cg_impl(const CoarseLevel& L, const void* bv, void* uv) {
@@ -504,7 +579,7 @@ struct Coarse {
       if (entry == 0) stage_in(0);
       if (rank == 0) by_prec(B.prec, [&](auto pc) { cg<decltype(pc)::value>(B, B.b, B.u); });
       __syncthreads();
-      if (!small(B)) grid_sync();
+      if (!small(B)) gsync();
       cur[0] = B.u;
       stamp(2, 0);
     }
@@ -515,7 +590,7 @@ struct Coarse {
       if (!small(L) && small(C)) {
         stage_out(l - 1, cur[l - 1]);  // CTA 0's shared-memory correction -> global
         cur[l - 1] = a.lv[l - 1].u;
-        grid_sync();
+        gsync();
       }
       if (in_team(L)) {
         by_prec(L.prec, [&](auto fp) {
@@ -559,7 +634,7 @@ __host__ __device__ inline size_t coarse_smem(const CoarseArgs& a) {
 }
 
 template <bool FTZ, bool FMA, bool ACC32, int UP>
-__global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a, int use_smem) {
+__global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a, int use_smem, int cluster) {
   __shared__ CoarseLevel table[kMaxCoarseLevels];
   __shared__ __half t16[kMaxCoarseLevels][27];
   __shared__ float t32[kMaxCoarseLevels][27];
@@ -595,7 +670,7 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
     for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32);
+  Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, cluster != 0);
   c.run();
 }
 
@@ -610,27 +685,68 @@ cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = smem;
   }
-  // grid: every co-resident CTA when the top level is a grid level, else one
+  // grid: one CTA when every level is a CTA-0 level; else one thread-block
+  // cluster (16 CTAs, hardware cluster barriers) when the top level is
+  // small enough, else every co-resident CTA as a cooperative grid
   const CoarseLevel& T = a.lv[a.nlev - 1];
+  const long long top_m = T.nodes - 2;
+  const long long top_n = T.dim == 3 ? top_m * top_m * top_m : top_m * top_m;
   unsigned grid = 1;
-  if (!small_level(T, a.cta_points)) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
-    grid = (unsigned)std::max(1, per) * (unsigned)std::max(1, sms);
-  }
+  int cluster = 0;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = dyn;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, use_smem);
+  if (!small_level(T, a.cta_points)) {
+    static int cl_env = -1;
+    if (cl_env < 0) {
+      const char* e = std::getenv("MPMG_COARSE_CLUSTER");
+      cl_env = e ? std::atoi(e) : 0;  // opt-in: measured slower than the cooperative grid
+    }
+    if (cl_env > 1 && top_n <= kClusterPoints) {
+      static int cl_size = -1;
+      if (cl_size < 0) {  // largest cluster (<= the request) that can be resident
+        cl_size = 0;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (int c = cl_env; c >= 2 && !cl_size; c /= 2) {
+          cudaLaunchConfig_t q = cfg;
+          q.gridDim = dim3(c);
+          cudaLaunchAttribute qa[1];
+          qa[0].id = cudaLaunchAttributeClusterDimension;
+          qa[0].val.clusterDim.x = c;
+          qa[0].val.clusterDim.y = 1;
+          qa[0].val.clusterDim.z = 1;
+          q.attrs = qa;
+          int nc = 0;
+          if (cudaOccupancyMaxActiveClusters(&nc, kern, &q) == cudaSuccess && nc > 0) cl_size = c;
+        }
+        cudaGetLastError();
+      }
+      if (cl_size > 1) cluster = cl_size;
+    }
+    if (cluster) {
+      grid = (unsigned)cluster;
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+    } else {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+      grid = (unsigned)std::max(1, per) * (unsigned)std::max(1, sms);
+    }
+  }
+  if (!cluster) {
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  }
+  cfg.gridDim = dim3(grid);
+  return cudaLaunchKernelEx(&cfg, kern, a, use_smem, cluster);
 }
 
 template <bool FTZ, bool FMA, bool ACC32>

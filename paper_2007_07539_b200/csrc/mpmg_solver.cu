@@ -29,7 +29,7 @@ bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("MPMG_PDL");
-    v = e ? std::atoi(e) : 1;
+    v = e ? std::atoi(e) : 0;  // off by default: no measured gain inside the graph
   }
   return v != 0;
 }
