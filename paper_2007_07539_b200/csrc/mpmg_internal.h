@@ -78,6 +78,10 @@ bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double*
                      const double* alpha_dev, double* partials, bool fma, cudaStream_t s, cudaError_t* err,
                      const mpmg_slab* slab = nullptr);
 int plane_partials(int dim, int nodes, int lp, bool update, int pz = 0);
+bool plane_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* r, const double* alpha_dev,
+                    double* partials, void* ring, long long ring_len, const int* slot, double* ring_scale, bool fma,
+                    cudaStream_t s, cudaError_t* err);
+int plane_update_r_partials(int dim, int nodes, int lp);
 // true when the streaming stencil kernels support this level shape
 bool stencil_supported(int dim, int nodes, int prec);
 
@@ -104,6 +108,8 @@ cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* 
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 cudaError_t launch_partials_sum(const double* partials, int n, double* out, cudaStream_t s);
 int norm2_partials(size_t len);
+cudaError_t launch_fold(size_t len, double* u, const void* ring, long long ring_len, int prec, const double* scales,
+                        const int* count, int extra, const int* gate, bool fma, cudaStream_t s);
 cudaError_t launch_fill_random01(double* padded_u, int dim, int nodes, uint64_t seed, cudaStream_t s);
 
 // ---- coarse sub-hierarchy (mpmg_coarse.cu) --------------------------------
@@ -141,6 +147,8 @@ struct IrState {
   int diverged;
   int active;         // loop still running
   int refresh_now;    // next refresh due
+  int pending;        // deferred corrections stored in the ring, not yet folded into u
+  int fold_now;       // the current iteration folds the ring into u (refresh due or ring full)
   int pad;
 };
 

@@ -35,7 +35,11 @@
 namespace mpmg_dev {
 
 enum { POP_SPMV = 0, POP_DEFECT = 1, POP_JACOBI = 2, POP_DEFECT64 = 3, POP_RESNORM = 4, POP_UPDATE = 5,
-       POP_JACOBI_Z = 6 };  // JACOBI_Z: steps 1 and 2 from u = 0 fused (operand = b, u1 = w D^-1 b on the fly)
+       POP_JACOBI_Z = 6, POP_UPDATE_R = 7 };
+// JACOBI_Z: steps 1 and 2 from u = 0 fused (operand = b, u1 = w D^-1 b on the fly)
+// UPDATE_R: the r half of UPDATE (r -= a A c) plus a copy of c into slot
+//   *ring_slot of the correction ring, whose u += a c updates are applied
+//   later in the same order (deferred correction, mpmg_solver.cu)
 
 struct PlaneArgs {
   int P;             // pitch
@@ -60,6 +64,10 @@ struct PlaneArgs {
   const double* alpha;  // UPDATE scale (device scalar)
   double* partials;     // per-CTA sum of squares (DEFECT64 / RESNORM / UPDATE)
   const int* gate;      // optional device flag: no-op unless *gate != 0
+  void* ring;           // UPDATE_R: correction ring (slots of ring_len values, precision LP)
+  long long ring_len;
+  const int* ring_slot; // UPDATE_R: device slot index
+  double* ring_scale;   // UPDATE_R: per-slot scale (= *alpha)
 };
 
 // ---- PTX: mbarrier + bulk copy ------------------------------------------
@@ -441,12 +449,13 @@ struct PlaneK {
   static constexpr int kThreads = 32 * WX * WY;
   static constexpr int TY = WY * RY;
   static constexpr bool kB = OP == POP_DEFECT || OP == POP_JACOBI || OP == POP_DEFECT64 || OP == POP_RESNORM;
-  static constexpr bool kNorm = OP == POP_DEFECT64 || OP == POP_RESNORM || OP == POP_UPDATE;
+  static constexpr bool kNorm = OP == POP_DEFECT64 || OP == POP_RESNORM || OP == POP_UPDATE || OP == POP_UPDATE_R;
   // binary16/32 level ops prefetch b into registers one plane ahead (global
   // loads); the FP64 epilogue operands are staged through shared memory
   static constexpr bool kBReg = (OP == POP_DEFECT || OP == POP_JACOBI) && EP != P64 && !(OPT & 1);
   static constexpr bool kJZ = OP == POP_JACOBI_Z;  // b is the stencil operand: nothing else staged
-  static constexpr int kEpiBytes = OP == POP_UPDATE ? 16 : ((kB && !kBReg) ? Bytes<EP>::v : 0);  // per value
+  static constexpr int kEpiBytes =
+      OP == POP_UPDATE ? 16 : (OP == POP_UPDATE_R ? 8 : ((kB && !kBReg) ? Bytes<EP>::v : 0));  // per value
   static constexpr int kP = 32 * WX * W;  // pitch (compile-time)
   static constexpr int kXRow = kP * Bytes<LP>::v;
   static constexpr int kXBytes = (TY + 2) * kXRow;
@@ -488,6 +497,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
     const uint32_t eb = (uint32_t)(erows * P * (K::kEpiBytes ? Bytes<EP>::v : 0));
     uint32_t tot = xb;
     if constexpr (OP == POP_UPDATE) tot += 2 * (uint32_t)(erows * P * 8);
+    else if constexpr (OP == POP_UPDATE_R) tot += (uint32_t)(erows * P * 8);
     else if constexpr (K::kB && !K::kBReg) tot += eb;
     mbar_arrive_tx(bar, tot);
     const long long xo = q * plane + (long long)(y0 - 1) * P;
@@ -496,20 +506,28 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
     if constexpr (OP == POP_UPDATE) {
       bulk_g2s(st + K::kXBytes, a.r64 + eo, (uint32_t)(erows * P * 8), bar);
       bulk_g2s(st + K::kXBytes + TY * P * 8, a.u64 + eo, (uint32_t)(erows * P * 8), bar);
+    } else if constexpr (OP == POP_UPDATE_R) {
+      bulk_g2s(st + K::kXBytes, a.r64 + eo, (uint32_t)(erows * P * 8), bar);
     } else if constexpr (K::kB && !K::kBReg) {
       bulk_g2s(st + K::kXBytes, static_cast<const unsigned char*>(a.b) + eo * Bytes<EP>::v, eb, bar);
     }
   };
 
+  pdl_wait();    // predecessor output visible from here on
+  pdl_launch();  // let the next kernel's CTAs be scheduled as ours retire
+  if (a.gate && *a.gate == 0) return;  // uniform across the grid
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
     fence_barrier_init();
   }
   __syncthreads();
-  pdl_wait();    // predecessor output visible from here on
-  pdl_launch();  // let the next kernel's CTAs be scheduled as ours retire
-  if (a.gate && *a.gate == 0) return;  // uniform across the grid
+  long long ring_off = 0;
+  if constexpr (OP == POP_UPDATE_R) {
+    const int slot = *a.ring_slot;
+    ring_off = (long long)slot * a.ring_len;
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) a.ring_scale[slot] = *a.alpha;
+  }
   if (tid == 0) {
     for (int k = 0; k < NS - 1 && k < NQ; ++k) issue(k);
   }
@@ -673,6 +691,21 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
           if (OP == POP_DEFECT64 && a.out) gstore<P64, W>(a.out, gi, r);
 #pragma unroll
           for (int e = 0; e < W; ++e) sq = __fma_rn(r.v[e], r.v[e], sq);
+        }
+      } else if constexpr (OP == POP_UPDATE_R) {
+        const double al = *a.alpha;
+        Row<P64, W> rr, rn;
+        Row<LP, W> craw;
+        rload<P64, P64, W>(st + K::kXBytes + (tr + i) * (P * 8) + x0 * 8, rr);
+        rload<LP, LP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, craw);
+#pragma unroll
+        for (int e = 0; e < W; ++e) rn.v[e] = fma64<FMA>(-al, t.v[e], rr.v[e]);
+        if (x0 == 0) rzero_first<P64, W>(rn);
+        if (v) {
+          gstore<P64, W>(a.r64, gi, rn);
+          gstore<LP, W>(a.ring, ring_off + gi, craw);  // c unchanged (x = 0 ghost is zero)
+#pragma unroll
+          for (int e = 0; e < W; ++e) sq = __fma_rn(rn.v[e], rn.v[e], sq);
         }
       } else if constexpr (OP == POP_UPDATE) {
         const double al = *a.alpha;

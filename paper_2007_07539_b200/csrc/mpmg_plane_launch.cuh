@@ -20,7 +20,7 @@ template <int LP, int CP, int OP, int P, int V = 0>
 struct PlaneCfg {
   static constexpr int W = P >= 256 ? 8 : P / 32;
   static constexpr int WX = P / (32 * W);
-  static constexpr bool kWide = CP == P64 || (CP == P32 && LP != P16) || OP == POP_UPDATE;
+  static constexpr bool kWide = CP == P64 || (CP == P32 && LP != P16) || OP == POP_UPDATE || OP == POP_UPDATE_R;
   // output rows per thread and warp-rows per CTA
   static constexpr int RY0 = kWide ? 2 : 4;
   static constexpr int WY0 = WX >= 4 ? 1 : (WX == 2 ? 2 : 4);
@@ -37,6 +37,16 @@ inline int plane_variant() {
     const char* e = std::getenv("MPMG_PLANE_VARIANT");
     v = e ? std::atoi(e) : 0;
     if (v < 0 || v > 5) v = 0;
+  }
+  return v;
+}
+
+inline int outer_waves() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_OUTER_WAVES");
+    v = e ? std::atoi(e) : 1;
+    if (v < 1 || v > 64) v = 1;
   }
   return v;
 }
@@ -86,7 +96,11 @@ struct PlaneLaunch {
       per_sm = n > 0 ? n : 1;
     }
     const int ytiles = (P - 1 + K::TY - 1) / K::TY;
-    const int cap = per_sm * plane_num_sms();
+    int cap = per_sm * plane_num_sms();
+    // FP64 outer kernels (no z-halo on their FP64 streams): several waves of
+    // shorter chunks even out the per-SM tail
+    if constexpr (OP == POP_UPDATE || OP == POP_UPDATE_R || OP == POP_DEFECT64 || OP == POP_RESNORM)
+      cap *= outer_waves();
     int chunks = cap / ytiles;
     if (chunks < 1) chunks = 1;
     if (chunks > pz - 1) chunks = pz - 1;

@@ -58,6 +58,40 @@ bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double*
   });
 }
 
+// r -= a A c (+ ||r||^2 partials) and c -> ring slot *slot (deferred
+// u += a c, see mpmg_solver.cu); binary16/32 c only
+bool plane_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* r, const double* alpha_dev,
+                    double* partials, void* ring, long long ring_len, const int* slot, double* ring_scale, bool fma,
+                    cudaStream_t s, cudaError_t* err) {
+  if (c_prec == MPMG_FP64 || !plane_outer_supported(A64.dim, A64.nodes) || !aligned16(c) || !aligned16(r) ||
+      !aligned16(ring) || (ring_len * mpmg_bytes_per_value(c_prec)) % 16 != 0)
+    return false;
+  PlaneArgs a = plane_args(A64);
+  a.x = c; a.r64 = r; a.alpha = alpha_dev; a.partials = partials;
+  a.ring = ring; a.ring_len = ring_len; a.ring_slot = slot; a.ring_scale = ring_scale;
+  return with_pitch(a.P, [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    auto go = [&](auto lpc) {
+      constexpr int L = decltype(lpc)::value;
+      *err = fma ? PlaneLaunch<L, P64, P64, POP_UPDATE_R, false, true, PP>::run(a, s)
+                 : PlaneLaunch<L, P64, P64, POP_UPDATE_R, false, false, PP>::run(a, s);
+    };
+    if (c_prec == MPMG_FP16) go(std::integral_constant<int, P16>{});
+    else go(std::integral_constant<int, P32>{});
+  });
+}
+
+int plane_update_r_partials(int dim, int nodes, int lp) {
+  if (!plane_outer_supported(dim, nodes) || lp == MPMG_FP64) return -1;
+  int n = -1;
+  with_pitch(pitch(nodes), [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    n = lp == MPMG_FP16 ? PlaneLaunch<P16, P64, P64, POP_UPDATE_R, false, true, PP>::partials()
+                        : PlaneLaunch<P32, P64, P64, POP_UPDATE_R, false, true, PP>::partials();
+  });
+  return n;
+}
+
 // partial sums written per launch: UPDATE with operand precision lp, or the
 // FP64 defect / residual norm (lp == FP64); -1 when not covered
 // (FMA on/off and DEFECT64/RESNORM instantiations share the shared-memory

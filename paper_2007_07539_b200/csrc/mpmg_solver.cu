@@ -67,7 +67,7 @@ struct Level {
 // applies ir_solver.cpp:95-120 to the device IR state
 __global__ void k_control(IrState* st, const double* p_main, int n_main, const double* p_ref, int n_ref,
                           double* hist, int hist_cap, double tol, int max_it, int scale_enabled, int refresh,
-                          int increment, cudaGraphConditionalHandle cond, int use_cond) {
+                          int increment, cudaGraphConditionalHandle cond, int use_cond, int ring_k) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // pdl_wait (mpmg_arith.cuh)
   __shared__ double red[kCtlThreads];
   const bool ref = increment && st->refresh_now;
@@ -83,6 +83,9 @@ __global__ void k_control(IrState* st, const double* p_main, int n_main, const d
   }
   if (threadIdx.x == 0) {
     const double alpha = sqrt(red[0]);
+    // deferred corrections: this iteration stored one more c in the ring,
+    // or folded all of them (and its own) into u
+    if (increment && ring_k > 0) st->pending = st->fold_now ? 0 : st->pending + 1;
     if (increment) st->iterations += 1;
     const int it = st->iterations;
     if (hist && it < hist_cap) hist[it] = alpha;
@@ -97,6 +100,9 @@ __global__ void k_control(IrState* st, const double* p_main, int n_main, const d
     }
     st->active = active;
     st->refresh_now = (refresh > 0 && (it + 1) % refresh == 0) ? 1 : 0;
+    // the next iteration folds the ring into u when it refreshes r = b - A u
+    // or when its c fills the last slot
+    st->fold_now = ring_k > 0 && (st->refresh_now || st->pending + 1 >= ring_k) ? 1 : 0;
     if (use_cond) cudaGraphSetConditional(cond, active ? 1u : 0u);
   }
 }
@@ -109,6 +115,8 @@ __global__ void k_state_reset(IrState* st) {
   st->diverged = 0;
   st->active = 0;
   st->refresh_now = 0;
+  st->pending = 0;
+  st->fold_now = 0;
 }
 
 __global__ void k_sanitize_scale(double* s) {
@@ -136,6 +144,16 @@ struct mpmg_solver {
   bool rlow_alias = false;
   double *partU = nullptr, *partD = nullptr;
   int nU = 0, nD = 0;
+  // deferred corrections (binary16/32 finest level): the r half of
+  // update_residuum_correction runs every iteration and parks c in a ring;
+  // u += a_k c_k is applied for all parked k at once, in order, when r is
+  // refreshed from u, when the ring is full and at the end of the solve --
+  // per element the same fma sequence, so u is bitwise unchanged, while each
+  // iteration skips the FP64 read + write of u (16 of 34 bytes per unknown)
+  int ring_k = 0;  // 0: fused update (FP64 finest level or unsupported shape)
+  void* ring = nullptr;
+  long long ring_len = 0;
+  double* ring_scale = nullptr;
   IrState* st = nullptr;
   IrState* st_h = nullptr;
   double* hist = nullptr;
@@ -256,7 +274,7 @@ struct mpmg_solver {
     if (e == cudaSuccess) {
       k_control<<<1, kCtlThreads, 0, q>>>(st, partD, nD, partD, nD, hist, hist_cap, p.outer_tolerance,
                                             p.max_outer_iterations, scale_enabled(p),
-                                            p.residual_refresh_interval, 0, h, use_cond);
+                                            p.residual_refresh_interval, 0, h, use_cond, ring_k);
       e = cudaGetLastError();
     }
     return e;
@@ -270,20 +288,30 @@ struct mpmg_solver {
       e = launch_downcast(cfg.dim, cfg.nodes, r, rlow, fp, &st->scale, 1, policy(), q);
     void* c = nullptr;
     if (e == cudaSuccess) e = v_cycle(q, &c);  // ir_solver.cpp:111
-    if (e == cudaSuccess)  // ir_solver.cpp:112
+    if (ring_k > 0) {  // ir_solver.cpp:112, the u half deferred
+      if (e == cudaSuccess && !plane_update_r(A64, c, fp, r, &st->scale, partU, ring, ring_len, &st->pending,
+                                              ring_scale, fma(), q, &e))
+        e = cudaErrorInvalidValue;
+      if (e == cudaSuccess)
+        e = launch_fold(len, u, ring, ring_len, fp, ring_scale, &st->pending, 1, &st->fold_now, fma(), q);
+    } else if (e == cudaSuccess) {  // ir_solver.cpp:112
       e = launch_update_rc(A64, c, fp, r, u, &st->scale, partU, fma(), q);
+    }
     if (e == cudaSuccess && p.residual_refresh_interval > 0)  // ir_solver.cpp:115-119 (gated on device)
       e = launch_defect64(A64, b, u, r, partD, fma(), false, q, &st->refresh_now);
     if (e == cudaSuccess) {
       e = launch_pdl(k_control, dim3(1), dim3(kCtlThreads), 0, q, st, (const double*)partU, nU,
                      (const double*)partD, nD, hist, hist_cap, p.outer_tolerance, p.max_outer_iterations,
-                     scale_enabled(p), p.residual_refresh_interval, 1, h, use_cond);
+                     scale_enabled(p), p.residual_refresh_interval, 1, h, use_cond, ring_k);
     }
     return e;
   }
 
   cudaError_t enqueue_final(cudaStream_t q) {  // residual_norm, ir_solver.cpp:21-49 / :122
-    cudaError_t e = launch_defect64(A64, b, u, nullptr, partD, true, true, q);
+    cudaError_t e = cudaSuccess;
+    if (ring_k > 0)  // corrections still parked
+      e = launch_fold(len, u, ring, ring_len, lv.back().A.prec, ring_scale, &st->pending, 0, nullptr, fma(), q);
+    if (e == cudaSuccess) e = launch_defect64(A64, b, u, nullptr, partD, true, true, q);
     if (e == cudaSuccess) e = launch_norm_finalize(partD, nD, final_d, q);
     return e;
   }
@@ -478,6 +506,17 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
   // partial-sum buffers
   S->nU = stencil_partials(c.dim, c.nodes, fprec, true);
   S->nD = stencil_partials(c.dim, c.nodes, MPMG_FP64, false);
+  if (env_ll("MPMG_DEFER_U", 1) != 0 && fprec != MPMG_FP64) {
+    const int nr = plane_update_r_partials(c.dim, c.nodes, fprec);
+    if (nr > 0) {
+      S->ring_k = 10;
+      S->nU = nr;
+      S->ring_len = (long long)((S->len + 63) / 64 * 64);
+    }
+  }
+  if (e == cudaSuccess && S->ring_k > 0)
+    e = S->alloc(&S->ring, (size_t)S->ring_k * (size_t)S->ring_len * (size_t)mpmg_bytes_per_value(fprec));
+  if (e == cudaSuccess && S->ring_k > 0) e = S->alloc(&S->ring_scale, (size_t)S->ring_k * 8);
   const int npart = std::max({S->nU, S->nD, norm2_partials(S->lv[F].len)});
   if (e == cudaSuccess) e = S->alloc(&S->partU, (size_t)npart * 8);
   if (e == cudaSuccess) e = S->alloc(&S->partD, (size_t)npart * 8);

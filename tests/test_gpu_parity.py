@@ -181,3 +181,31 @@ def test_scaling_forced_off_stagnates_h_mg():
     _, on = h.ir_solve(b, mg.IrConfig(outer_tolerance=1e-9, max_outer_iterations=40))
     _, off = h.ir_solve(b, mg.IrConfig(outer_tolerance=1e-9, max_outer_iterations=40, scaling=2))
     assert on.converged and not off.converged
+
+
+@pytest.mark.parametrize("variant,refresh,max_it,tol", [
+    ("h_mg", 10, 100, 1e-10),   # the benchmark schedule: one fold at the refresh
+    ("h_mg", 3, 100, 1e-10),    # a fold every 3 iterations
+    ("hsd_mg", 0, 14, 1e-30),   # no refresh: folds when the 10-slot ring fills, then at the end
+    ("h_mg", 10, 14, 1e-30),    # fold at 10, 4 parked corrections folded after the loop
+])
+@pytest.mark.parametrize("graph", [True, False])
+def test_deferred_corrections_bitwise(variant, refresh, max_it, tol, graph, monkeypatch):
+    """The deferred u += a c (ring of parked corrections, mpmg_solver.cu) gives
+    the bitwise solution, residual history and iteration count of the fused
+    per-iteration update_residuum_correction (kernels.cpp:300-341)."""
+    dim, n, L = 3, 65, 6
+    b = mg.problem_rhs(dim, n)
+    out = []
+    for defer in ("1", "0"):
+        monkeypatch.setenv("MPMG_DEFER_U", defer)
+        h = mg.Hierarchy(dim, n, L, variant, ftz=False)
+        cfg = mg.IrConfig(outer_tolerance=tol * float(np.linalg.norm(b)), max_outer_iterations=max_it,
+                          residual_refresh_interval=refresh, use_graph=graph)
+        out.append(h.ir_solve(b, cfg))
+        h.close()
+    (u1, r1), (u0, r0) = out
+    assert r1.iterations == r0.iterations and r1.converged == r0.converged
+    assert same(u1.view(np.uint64), u0.view(np.uint64))
+    assert same(r1.residual_history, r0.residual_history)
+    assert r1.final_residual == r0.final_residual
