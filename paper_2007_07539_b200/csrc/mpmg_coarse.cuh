@@ -219,9 +219,14 @@ struct Coarse {
 
   template <typename F>
   __device__ void for_points(const CoarseLevel& L, F&& f) {
+    for_points_by(L, !small(L), f);
+  }
+  // grid: the points are spread over every CTA (else each CTA walks all of them)
+  template <typename F>
+  __device__ void for_points_by(const CoarseLevel& L, bool grid, F&& f) {
     const Pt p = points(L);
     int start = threadIdx.x, stride = blockDim.x;
-    if (!small(L)) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
+    if (grid) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
     for (int k = start; k < p.n; k += stride) f(p.idx(k), p.P);
   }
 
@@ -266,14 +271,20 @@ struct Coarse {
 
   // R r_f (product in the fine precision FP) -> coarse b; when `keep`, the
   // binary64 products go to C.prod first (DSH rescale norm)
+  // A grid level restricting into a CTA-0 level (the entry level) spreads
+  // the coarse points over the grid and writes the global copy of C.b, which
+  // stage_in then brings into CTA 0's shared memory.
   template <int FP>
-  __device__ void restrict_to(const CoarseLevel& F, const CoarseLevel& C, const void* rfv, bool keep) {
+  __device__ void restrict_to(const CoarseLevel& F, const CoarseLevel& Cin, const void* rfv, bool keep) {
     using OF = O<FP>;
     using T = typename OF::T;
     const T* rf = static_cast<const T*>(rfv);
     const int Pf = F.nodes - 1;
     const int pf = F.dim == 3 ? Pf * Pf : 0;
-    for_points(C, [&](int ci, int Pc) {
+    const bool spread = !keep && !small(F) && small(Cin);
+    const CoarseLevel& C = Cin;
+    void* const cb = spread ? a.lv[&Cin - lv].b : C.b;
+    for_points_by(C, spread || !small(C), [&](int ci, int Pc) {
       const int cx = ci % Pc, cy = (ci / Pc) % Pc, cz = F.dim == 3 ? ci / (Pc * Pc) : 0;
       const int cf = cz * 2 * pf + cy * 2 * Pf + cx * 2;
       T acc = OF::zero();
@@ -285,7 +296,7 @@ struct Coarse {
       if (keep) C.prod[ci] = OF::wide(acc);
       else by_prec(C.prec, [&](auto cp) {
         using OC = O<decltype(cp)::value>;
-        static_cast<typename OC::T*>(C.b)[ci] = OC::from(OF::wide(acc));  // scale 1
+        static_cast<typename OC::T*>(cb)[ci] = OC::from(OF::wide(acc));  // scale 1
       });
     });
   }
@@ -539,8 +550,10 @@ struct Coarse {
         u = L.u;
       }
       cur[l] = u;
+      stamp(4, l);
       if (in_team(L)) by_prec(L.prec, [&](auto pc) { defect<decltype(pc)::value>(L, L.b, u, L.r); });
       sync(L);
+      stamp(5, l);
       const bool rescale = a.rescale && C.prec == MPMG_FP16;  // multigrid.cpp:383
       if (in_team(L)) by_prec(L.prec, [&](auto pc) { restrict_to<decltype(pc)::value>(L, C, L.r, rescale); });
       sync(L);
@@ -600,6 +613,7 @@ struct Coarse {
         });
       }
       sync(L);
+      stamp(6, l);
       void* u = smooth(L, cur[l], a.post);
       if (l == top && u != a.lv[top].u) {  // the caller reads the top correction from global L.u
         if (in_team(L)) copy_level(L, u, a.lv[top].u);
@@ -738,6 +752,12 @@ cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+      static int per_env = -1;  // MPMG_COARSE_PER_SM: CTAs per SM (<= occupancy)
+      if (per_env < 0) {
+        const char* e = std::getenv("MPMG_COARSE_PER_SM");
+        per_env = e ? std::atoi(e) : 0;
+      }
+      if (per_env > 0) per = std::min(per, per_env);
       grid = (unsigned)std::max(1, per) * (unsigned)std::max(1, sms);
     }
   }

@@ -108,6 +108,7 @@ cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* 
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 cudaError_t launch_partials_sum(const double* partials, int n, double* out, cudaStream_t s);
 int norm2_partials(size_t len);
+cudaError_t launch_copy_sumsq(size_t len, const double* x, double* y, double* partials, cudaStream_t s);
 cudaError_t launch_fold(size_t len, double* u, const void* ring, long long ring_len, int prec, const double* scales,
                         const int* count, int extra, const int* gate, bool fma, cudaStream_t s);
 cudaError_t launch_fill_random01(double* padded_u, int dim, int nodes, uint64_t seed, cudaStream_t s);

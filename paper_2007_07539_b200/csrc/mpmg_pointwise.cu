@@ -322,6 +322,23 @@ __global__ void k_jacobi_zero8(const void* __restrict__ bv, void* __restrict__ u
   }
 }
 
+template <typename T>
+__device__ __forceinline__ void ldg4(const T* p, T* out) {
+  if constexpr (sizeof(T) == 2) {
+    const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+    out[0] = __ushort_as_half((unsigned short)(q.x & 0xFFFFu));
+    out[1] = __ushort_as_half((unsigned short)(q.x >> 16));
+    out[2] = __ushort_as_half((unsigned short)(q.y & 0xFFFFu));
+    out[3] = __ushort_as_half((unsigned short)(q.y >> 16));
+  } else if constexpr (sizeof(T) == 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    out[0] = q.x; out[1] = q.y; out[2] = q.z; out[3] = q.w;
+  } else {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
+  }
+}
+
 // prolongation + correction, 8 consecutive fine x per thread (Pf % 8 == 0);
 // same parent order and rounding as k_prolong
 template <int DIM, int FP, int CPc, bool FTZ, bool FMA>
@@ -351,8 +368,10 @@ __global__ void k_prolong8(const void* __restrict__ cc_, void* __restrict__ uf_,
     for (int j = 0; j < 2; ++j) {
       if (k < nz && j < ny) {
         const long long base = (DIM == 3 ? (long long)pz[k] * Pc * Pc : 0) + (long long)py[j] * Pc + x0 / 2;
-#pragma unroll
-        for (int e = 0; e < 5; ++e) c[k][j][e] = (x0 / 2 + e <= Pc) ? __ldg(cc + base + e) : X::zero();
+        // x0/2 is a multiple of 4: one aligned 4-value load + one scalar
+        // (x0/2 + 4 <= Pc always; index Pc is the row's aliased zero ghost)
+        ldg4<TC>(cc + base, c[k][j]);
+        c[k][j][4] = __ldg(cc + base + 4);
       }
     }
   const double s = scale_dev ? *scale_dev : 1.0;
@@ -465,6 +484,36 @@ __global__ void k_sumsq(const double* __restrict__ x, long long len, double* par
   double acc = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
     acc = __fma_rn(x[i], x[i], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+// r = b and per-block sums of b_i^2: the initial defect b - A u for u = 0
+// (ir_solver.cpp:92-93) bitwise -- t = A 0 = +0 and fma(-1, +0, b) = b for
+// every b including signed zeros -- at 16 instead of 24 bytes per unknown
+__global__ void k_copy_sumsq(const double* __restrict__ x, double* __restrict__ y, long long len,
+                             double* partials) {
+  __shared__ double red[kThreads / 32];
+  double acc = 0.0;
+  const long long n2 = len / 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+    const double2 v = reinterpret_cast<const double2*>(x)[i];
+    reinterpret_cast<double2*>(y)[i] = v;
+    acc = __fma_rn(v.x, v.x, acc);
+    acc = __fma_rn(v.y, v.y, acc);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (len & 1)) {
+    const double v = x[len - 1];
+    y[len - 1] = v;
+    acc = __fma_rn(v, v, acc);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -595,7 +644,7 @@ cudaError_t launch_prolong(int dim, int fine_nodes, int fine_prec, int coarse_pr
   const int Pf = pitch(fine_nodes);
   const dim3 block(32, 8);
   const dim3 grid((Pf - 1 + 31) / 32, (Pf - 1 + 7) / 8, dim == 3 ? Pf - 1 : 1);
-  const bool vec = Pf % 8 == 0 && aligned64(u_fine);
+  const bool vec = Pf % 8 == 0 && aligned64(u_fine) && ((uintptr_t)c_coarse & 15u) == 0;
   const dim3 grid8v((unsigned)(((Pf / 8) * (Pf - 1) + kThreads - 1) / kThreads), dim == 3 ? Pf - 1 : 1);
   return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
     return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
@@ -649,7 +698,7 @@ cudaError_t launch_prolong_slab(int fine_nodes, const mpmg_slab& sf, const mpmg_
                                 int coarse_prec, const void* c_coarse, void* u_fine, uint32_t policy,
                                 cudaStream_t s) {
   const int Pf = pitch(fine_nodes);
-  if (Pf % 8 || !aligned64(u_fine) || sf.nz < 1) return cudaErrorInvalidValue;
+  if (Pf % 8 || !aligned64(u_fine) || ((uintptr_t)c_coarse & 15u) || sf.nz < 1) return cudaErrorInvalidValue;
   const dim3 grid8v((unsigned)(((Pf / 8) * (Pf - 1) + kThreads - 1) / kThreads), sf.nz);
   return with_prec(fine_prec, [&](auto fp) -> cudaError_t {
     return with_prec(coarse_prec, [&](auto cp) -> cudaError_t {
@@ -751,6 +800,12 @@ cudaError_t launch_norm2(size_t len, const double* x, double* partials, double* 
   const int nb = norm2_partials(len);
   k_sumsq<<<nb, kThreads, 0, s>>>(x, (long long)len, partials);
   k_finalize<<<1, kThreads, 0, s>>>(partials, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_sumsq(size_t len, const double* x, double* y, double* partials, cudaStream_t s) {
+  if (((uintptr_t)x & 15u) || ((uintptr_t)y & 15u)) return cudaErrorInvalidValue;
+  k_copy_sumsq<<<norm2_partials(len), kThreads, 0, s>>>(x, y, (long long)len, partials);
   return cudaGetLastError();
 }
 

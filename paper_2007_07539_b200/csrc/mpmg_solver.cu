@@ -270,9 +270,14 @@ struct mpmg_solver {
     if (e == cudaSuccess) e = cudaMemsetAsync(u, 0, len * sizeof(double), q);
     if (e == cudaSuccess && p.random_initial_guess)
       e = launch_fill_random01(u, cfg.dim, cfg.nodes, p.seed, q);
-    if (e == cudaSuccess) e = launch_defect64(A64, b, u, r, partD, fma(), false, q);  // ir_solver.cpp:92-93
+    int n0 = nD;  // ir_solver.cpp:92-93: r = b - A u
+    if (e == cudaSuccess && p.random_initial_guess) e = launch_defect64(A64, b, u, r, partD, fma(), false, q);
+    else if (e == cudaSuccess) {  // u = 0: r = b bitwise
+      e = launch_copy_sumsq(len, b, r, partD, q);
+      n0 = norm2_partials(len);
+    }
     if (e == cudaSuccess) {
-      k_control<<<1, kCtlThreads, 0, q>>>(st, partD, nD, partD, nD, hist, hist_cap, p.outer_tolerance,
+      k_control<<<1, kCtlThreads, 0, q>>>(st, partD, n0, partD, n0, hist, hist_cap, p.outer_tolerance,
                                             p.max_outer_iterations, scale_enabled(p),
                                             p.residual_refresh_interval, 0, h, use_cond, ring_k);
       e = cudaGetLastError();
@@ -536,7 +541,9 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
     A.base_tol = c.base_tol;
     A.base_mode = c.base_mode;
     A.base_maxit = c.base_max_iterations;
-    A.cta_points = (int)env_ll("MPMG_CTA_POINTS", 4096);
+    // levels up to 512 unknowns (7^3) run on CTA 0 out of shared memory; a
+    // grid-wide step (barrier-bound, ~2.5 us) beats one SM from 15^3 up
+    A.cta_points = (int)env_ll("MPMG_CTA_POINTS", 512);
     A.debug = (int)env_ll("MPMG_COARSE_DEBUG", 0);
     A.dbg = nullptr;
     if (A.debug) e = S->alloc(&A.dbg, 64 * sizeof(long long));
