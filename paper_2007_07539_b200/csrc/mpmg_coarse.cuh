@@ -36,8 +36,6 @@ using namespace mpmg_dev;
 namespace coarse_detail {
 
 constexpr int kThreads = 512;
-// top levels up to this many unknowns run on one 16-CTA cluster
-constexpr long long kClusterPoints = 65536;
 constexpr int kCtaPoints = 4096;
 
 template <int PR> struct T_;
@@ -172,6 +170,37 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
+// ---- cluster slab mode ----------------------------------------------------
+// One thread-block cluster of C CTAs runs the coarse cycle with every level
+// above the CTA-0 levels split into z-slabs that live in the CTAs' shared
+// memory (one halo plane each side, pushed to the neighbours through
+// distributed shared memory after every operation) -- an operation is local
+// shared-memory work plus one hardware cluster barrier instead of L2 round
+// trips plus a grid-wide barrier. Ownership nests: CTA r owns planes
+// [lo_T(r), lo_T(r+1)) of the top level T, lo_T(r) = 1 + r (P_T - 1) / C, and
+// coarse plane k wherever it owns fine plane 2k: lo_l(r) = ceil(lo_T(r) / 2^(T-l)).
+__host__ __device__ inline int slab_lo(int P_top, int C, int shift, int r) {
+  const int lt = 1 + (r * (P_top - 1)) / C;
+  return (lt + (1 << shift) - 1) >> shift;
+}
+// elements of one slab buffer of a level with pitch P and at most nz owned planes
+__host__ __device__ inline long long slab_elems(int P, int nz) { return (long long)(nz + 3) * P * P; }
+__host__ __device__ inline int slab_max_nz(int P_top, int C, int shift) {
+  int m = 0;
+  for (int r = 0; r < C; ++r) {
+    const int nz = slab_lo(P_top, C, shift, r + 1) - slab_lo(P_top, C, shift, r);
+    m = nz > m ? nz : m;
+  }
+  return m;
+}
+
+// halo pushes of one CTA on one slab level: plane src (local plane index) to
+// CTA t's local plane dst; CTA t reads planes lo_t - 1 and hi_t
+struct PushTab {
+  int n;
+  signed char t[8], src[8], dst[8];
+};
+
 // UP: the one precision of every level (P16/P32/P64: H_MG, D_MG -- a single
 // code path, a third of the instruction footprint), or 3 for mixed cascades
 template <bool FTZ, bool FMA, bool ACC32, int UP>
@@ -182,14 +211,20 @@ struct Coarse {
   void* const* cgp;  // CG scratch r, p, ap, s, best
   const __half (*t16)[27];
   const float (*t32)[27];
-  const bool clustered;  // the grid is one thread-block cluster (else a cooperative grid)
+  const bool slab;  // cluster slab mode (else a cooperative grid, level data in global memory)
   __device__ Coarse(const CoarseArgs& args, CoarseLevel* table, void* const* cg, const __half (*a16)[27],
                     const float (*a32)[27], bool cluster)
-      : a(args), rank(blockIdx.x), ncta(gridDim.x), lv(table), cgp(cg), t16(a16), t32(a32), clustered(cluster) {}
+      : a(args), rank(blockIdx.x), ncta(gridDim.x), lv(table), cgp(cg), t16(a16), t32(a32), slab(cluster) {}
   __device__ void gsync() {
-    if (clustered) cluster_sync();
+    if (slab) cluster_sync();
     else grid_sync();
   }
+  // slab mode: owned planes [lo(l, r), lo(l, r + 1)) of level l (table in
+  // shared memory, filled at kernel start)
+  const short (*slo)[17] = nullptr;
+  const PushTab* push = nullptr;  // per level: planes this CTA pushes, and to whom
+  __device__ int lo(int l, int r) const { return slo[l][r]; }
+
   template <int PR>
   __device__ typename Lv<PR, FTZ, FMA, ACC32>::Taps taps_of(const CoarseLevel& L) const {
     const int l = (int)(&L - lv);
@@ -203,12 +238,14 @@ struct Coarse {
   int nst = 0;
   // phase timestamps (MPMG_COARSE_DEBUG): code*1e12 + cycles since start,
   // kept in registers by thread 0 of CTA 0 and written to a.dbg at the end
+  // (MPMG_COARSE_DEBUG = 3 + r records CTA r's stamps, with the fine-grained ones)
+  __device__ unsigned stamp_rank() const { return a.debug >= 3 ? (unsigned)(a.debug - 3) : 0u; }
   __device__ void stamp(int code, int l) {
-    if (a.dbg && rank == 0 && threadIdx.x == 0 && nst < 63)
+    if (a.dbg && rank == stamp_rank() && threadIdx.x == 0 && nst < 63)
       a.dbg[1 + nst++] = (long long)(code * 100 + l) * 1000000000000LL + (clock64() - t0);
   }
   __device__ void stamps_done() {
-    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[0] = nst;
+    if (a.dbg && rank == stamp_rank() && threadIdx.x == 0) a.dbg[0] = nst;
   }
   // team of a level: the whole grid, or CTA 0 alone
   __device__ bool in_team(const CoarseLevel& L) const { return !small(L) || rank == 0; }
@@ -219,15 +256,54 @@ struct Coarse {
 
   template <typename F>
   __device__ void for_points(const CoarseLevel& L, F&& f) {
-    for_points_by(L, !small(L), f);
+    for_points_by(L, small(L) ? 0 : (slab ? 2 : 1), f);
   }
-  // grid: the points are spread over every CTA (else each CTA walks all of them)
+  // mode 0: each CTA walks every point; 1: the points are spread over the
+  // grid; 2 (slab mode): this CTA's planes
   template <typename F>
-  __device__ void for_points_by(const CoarseLevel& L, bool grid, F&& f) {
+  __device__ void for_points_by(const CoarseLevel& L, int mode, F&& f) {
     const Pt p = points(L);
-    int start = threadIdx.x, stride = blockDim.x;
-    if (grid) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
-    for (int k = start; k < p.n; k += stride) f(p.idx(k), p.P);
+    int start = threadIdx.x, stride = blockDim.x, end = p.n;
+    if (mode == 1) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
+    if (mode == 2) {
+      const int l = (int)(&L - lv);
+      const int m2 = p.m * p.m;
+      start += (lo(l, (int)rank) - 1) * m2;
+      end = (lo(l, (int)rank + 1) - 1) * m2;
+    }
+    for (int k = start; k < end; k += stride) f(p.idx(k), p.P);
+  }
+  // slab mode: push this CTA's first / last owned plane of buffer x (level l)
+  // into the halo planes of every CTA that reads it -- CTA t reads planes
+  // lo_t - 1 and hi_t (also when its own slab is empty) -- then a cluster
+  // barrier. Halo planes outside 1..P-1 are ghost planes and stay zero.
+  __device__ void exchange(int l, void* x) {
+    const CoarseLevel& L = lv[l];
+    const int P = L.nodes - 1;
+    const int bytes = L.prec == MPMG_FP16 ? 2 : (L.prec == MPMG_FP32 ? 4 : 8);
+    const int pl = P * P * bytes;  // plane bytes (a multiple of 16)
+    const int zlo = lo(l, (int)rank);
+    __syncthreads();
+    const int cnt = push[l].n;
+    if (cnt > 0) {
+      // shared-window addresses: ld.shared locally, st.shared::cluster remotely
+      const uint32_t real = (uint32_t)__cvta_generic_to_shared(static_cast<unsigned char*>(x) + (long long)(zlo - 1) * pl);
+      const int n16 = pl / 16;
+      for (int i = threadIdx.x; i < cnt * n16; i += blockDim.x) {
+        const int k = i / n16, c = i - k * n16;
+        uint32_t dst;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(dst) : "r"(real + (uint32_t)push[l].dst[k] * (uint32_t)pl), "r"((int)push[l].t[k]));
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(real + (uint32_t)push[l].src[k] * (uint32_t)pl + 16u * c));
+        asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};"
+                     :: "r"(dst + 16u * c), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+      }
+    }
+    if (a.debug > 1) stamp(9, l);
+    cluster_sync();
   }
 
   template <typename F>
@@ -281,10 +357,13 @@ struct Coarse {
     const T* rf = static_cast<const T*>(rfv);
     const int Pf = F.nodes - 1;
     const int pf = F.dim == 3 ? Pf * Pf : 0;
-    const bool spread = !keep && !small(F) && small(Cin);
+    const bool spread = !keep && !small(F) && small(Cin) && !slab;
     const CoarseLevel& C = Cin;
     void* const cb = spread ? a.lv[&Cin - lv].b : C.b;
-    for_points_by(C, spread || !small(C), [&](int ci, int Pc) {
+    // slab mode: coarse plane k is computed by the owner of fine plane 2k
+    // (and written to CTA 0's shared memory when the coarse level is a CTA-0 level)
+    const int mode = (slab && !small(F)) ? 2 : ((spread || !small(C)) ? 1 : 0);
+    for_points_by(C, mode, [&](int ci, int Pc) {
       const int cx = ci % Pc, cy = (ci / Pc) % Pc, cz = F.dim == 3 ? ci / (Pc * Pc) : 0;
       const int cf = cz * 2 * pf + cy * 2 * Pf + cx * 2;
       T acc = OF::zero();
@@ -497,13 +576,25 @@ struct Coarse {
     });
   }
 
+  // barrier after an operation on level L that wrote buffer x (slab mode:
+  // halo exchange + cluster barrier for a slab level)
+  __device__ void after(const CoarseLevel& L, void* x) {
+    if (slab && !small(L)) {
+      if (a.debug > 1) { __syncthreads(); stamp(7, (int)(&L - lv)); }
+      exchange((int)(&L - lv), x);
+      if (a.debug > 1) stamp(8, (int)(&L - lv));
+    } else {
+      sync(L);
+    }
+  }
+
   // ping-pong smoothing between L.u and L.u2; returns the result buffer
   __device__ void* smooth(const CoarseLevel& L, void* cur, int steps) {
     for (int s = 0; s < steps; ++s) {
       void* out = (cur == L.u) ? L.u2 : L.u;
       const bool z = cur == nullptr;
       if (in_team(L)) by_prec(L.prec, [&](auto pc) { jacobi<decltype(pc)::value>(L, L.b, z ? L.b : cur, out, z); });
-      sync(L);
+      after(L, out);
       cur = out;
     }
     return cur;
@@ -524,6 +615,61 @@ struct Coarse {
   __device__ void stage_out(int l, const void* src) {
     if (rank == 0) copy_level(lv[l], src, a.lv[l].u);
     __syncthreads();
+  }
+
+  // slab mode schedule (3D, one precision, no DSH rescaling, level 0 a CTA-0 level)
+  __device__ void run_slab() {
+    void* cur[kMaxCoarseLevels];
+    const int top = a.nlev - 1;
+    t0 = clock64();
+    cluster_sync();  // every CTA's shared memory is laid out and zeroed
+    copy_level(lv[top], a.lv[top].b, lv[top].b);  // own planes of the top rhs
+    __syncthreads();
+    for (int l = top; l >= 1; --l) {
+      const CoarseLevel& L = lv[l];
+      const CoarseLevel& C = lv[l - 1];
+      stamp(1, l);
+      void* u = smooth(L, nullptr, a.pre);
+      if (u == nullptr) {  // pre_steps == 0: u = 0
+        if (in_team(L)) for_points(L, [&](int i, int) {
+          if (L.prec == MPMG_FP16) static_cast<uint16_t*>(L.u)[i] = 0;
+          else if (L.prec == MPMG_FP32) static_cast<float*>(L.u)[i] = 0.f;
+          else static_cast<double*>(L.u)[i] = 0.0;
+        });
+        after(L, L.u);
+        u = L.u;
+      }
+      cur[l] = u;
+      stamp(4, l);
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { defect<decltype(pc)::value>(L, L.b, u, L.r); });
+      after(L, L.r);
+      stamp(5, l);
+      if (in_team(L)) by_prec(L.prec, [&](auto pc) { restrict_to<decltype(pc)::value>(L, C, L.r, false); });
+      if (small(L)) __syncthreads();
+      else cluster_sync();  // coarse rhs complete (a CTA-0 level's in CTA 0)
+    }
+    if (rank == 0) by_prec(lv[0].prec, [&](auto pc) { cg<decltype(pc)::value>(lv[0], lv[0].b, lv[0].u); });
+    __syncthreads();
+    cur[0] = lv[0].u;
+    stamp(2, 0);
+    for (int l = 1; l <= top; ++l) {
+      const CoarseLevel& L = lv[l];
+      const CoarseLevel& C = lv[l - 1];
+      if (!small(L) && small(C)) cluster_sync();  // CTA 0's correction visible cluster-wide
+      if (in_team(L)) {
+        by_prec(L.prec, [&](auto fp) {
+          by_prec(C.prec, [&](auto cp) {
+            prolong<decltype(fp)::value, decltype(cp)::value>(L, C, cur[l - 1], cur[l], 1.0);
+          });
+        });
+      }
+      after(L, cur[l]);
+      stamp(6, l);
+      cur[l] = smooth(L, cur[l], a.post);
+      stamp(3, l);
+    }
+    copy_level(lv[top], cur[top], a.lv[top].u);  // own planes of the top correction
+    stamps_done();
   }
 
   __device__ void run() {
@@ -647,6 +793,28 @@ __host__ __device__ inline size_t coarse_smem(const CoarseArgs& a) {
   return n;
 }
 
+// slab mode shared-memory layout (identical in every CTA of the cluster):
+// per level, CTA-0 levels as full padded vectors and slab levels as C-way
+// z-slabs, 4 buffers each (u, u2, b, r), then the CG scratch of level 0.
+// off[l] = byte offset of level l's buffers, sz[l] = bytes per buffer.
+__host__ __device__ inline size_t slab_smem(const CoarseArgs& a, int C, size_t* off, size_t* sz) {
+  size_t n = 0;
+  const int T = a.nlev - 1;
+  for (int l = 0; l < a.nlev; ++l) {
+    const CoarseLevel& L = a.lv[l];
+    const long long P = L.nodes - 1;
+    long long elems = padded_of(L);
+    if (!small_level(L, a.cta_points)) elems = slab_elems((int)P, slab_max_nz((int)(a.lv[T].nodes - 1), C, T - l));
+    const size_t b = ((size_t)elems * bytes_of(L.prec) + 15) / 16 * 16;
+    if (off) off[l] = n;
+    if (sz) sz[l] = b;
+    n += 4 * b;
+  }
+  if (off) off[a.nlev] = n;
+  n += 5 * ((padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16);
+  return n;
+}
+
 template <bool FTZ, bool FMA, bool ACC32, int UP>
 __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a, int use_smem, int cluster) {
   __shared__ CoarseLevel table[kMaxCoarseLevels];
@@ -679,94 +847,159 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
     }
   }
   __syncthreads();
+  __shared__ short slo_tab[kMaxCoarseLevels][17];
+  __shared__ PushTab push_tab[kMaxCoarseLevels];
+  if (cluster) {  // slab mode: every CTA lays out its slabs (and CTA 0's levels)
+    for (int i = threadIdx.x; i < a.nlev * 17; i += blockDim.x) {
+      const int T = a.nlev - 1, l = i / 17, r = i % 17;
+      slo_tab[l][r] = (short)(r <= (int)gridDim.x ? slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, r) : 0);
+    }
+    if (threadIdx.x == 0) {
+      size_t off[kMaxCoarseLevels + 1], sz[kMaxCoarseLevels];
+      slab_smem(a, (int)gridDim.x, off, sz);
+      cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+      const int T = a.nlev - 1;
+      for (int l = 0; l < a.nlev; ++l) {
+        unsigned char* q[4];
+        for (int k = 0; k < 4; ++k) q[k] = dyn + off[l] + k * sz[l];
+        if (small_level(a.lv[l], a.cta_points)) {  // CTA 0's full vectors, reached through DSMEM
+          for (int k = 0; k < 4; ++k) q[k] = static_cast<unsigned char*>(cl.map_shared_rank((void*)q[k], 0));
+        } else {  // virtual base: global plane z of the slab at base + z * plane bytes
+          const long long P = a.lv[l].nodes - 1;
+          const long long shift = (long long)(slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, blockIdx.x) - 1) *
+                                  P * P * bytes_of(a.lv[l].prec);
+          for (int k = 0; k < 4; ++k) q[k] -= shift;
+        }
+        table[l].u = q[0]; table[l].u2 = q[1]; table[l].b = q[2]; table[l].r = q[3];
+      }
+      const size_t b0 = (padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16;
+      for (int k = 0; k < 5; ++k) cg[k] = dyn + off[a.nlev] + k * b0;
+    }
+    const size_t n = slab_smem(a, (int)gridDim.x, nullptr, nullptr) / 16;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (threadIdx.x < a.nlev) {  // push tables
+      const int l = threadIdx.x, C = (int)gridDim.x, r = blockIdx.x;
+      PushTab pt{};
+      const int zlo = slo_tab[l][r], zhi = slo_tab[l][r + 1];
+      if (!small_level(a.lv[l], a.cta_points))
+        for (int t = 0; t < C; ++t) {
+          if (t == r) continue;
+          const int tlo = slo_tab[l][t], thi = slo_tab[l][t + 1];
+          for (int side = 0; side < 2; ++side) {
+            const int z = side == 0 ? tlo - 1 : thi;
+            if (z < zlo || z >= zhi || pt.n >= 8) continue;
+            pt.t[pt.n] = (signed char)t;
+            pt.src[pt.n] = (signed char)(z - (zlo - 1));
+            pt.dst[pt.n] = (signed char)(z - (tlo - 1));
+            ++pt.n;
+          }
+        }
+      push_tab[l] = pt;
+    }
+    __syncthreads();
+    Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, true);
+    c.slo = slo_tab;
+    c.push = push_tab;
+    c.run_slab();
+    return;
+  }
   if (use_smem && blockIdx.x == 0) {  // ghosts must read as zero
     const size_t n = coarse_smem(a) / 16;
     for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, cluster != 0);
+  Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, false);
   c.run();
 }
 
 template <bool FTZ, bool FMA, bool ACC32, int UP>
 cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
   auto kern = k_coarse<FTZ, FMA, ACC32, UP>;
-  const size_t smem = coarse_smem(a);
-  const int use_smem = smem <= 200 * 1024 ? 1 : 0;
-  const size_t dyn = use_smem ? smem : 0;
-  static size_t attr_set = 0;
-  if (use_smem && smem > attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = smem;
-  }
-  // grid: one CTA when every level is a CTA-0 level; else one thread-block
-  // cluster (16 CTAs, hardware cluster barriers) when the top level is
-  // small enough, else every co-resident CTA as a cooperative grid
   const CoarseLevel& T = a.lv[a.nlev - 1];
-  const long long top_m = T.nodes - 2;
-  const long long top_n = T.dim == 3 ? top_m * top_m * top_m : top_m * top_m;
-  unsigned grid = 1;
-  int cluster = 0;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = dyn;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (!small_level(T, a.cta_points)) {
-    static int cl_env = -1;
-    if (cl_env < 0) {
-      const char* e = std::getenv("MPMG_COARSE_CLUSTER");
-      cl_env = e ? std::atoi(e) : 0;  // opt-in: measured slower than the cooperative grid
+  static size_t attr_set = 0;
+  auto want_smem = [&](size_t bytes) {
+    if (bytes > attr_set) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      attr_set = bytes;
     }
-    if (cl_env > 1 && top_n <= kClusterPoints) {
-      static int cl_size = -1;
-      if (cl_size < 0) {  // largest cluster (<= the request) that can be resident
-        cl_size = 0;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        for (int c = cl_env; c >= 2 && !cl_size; c /= 2) {
-          cudaLaunchConfig_t q = cfg;
-          q.gridDim = dim3(c);
-          cudaLaunchAttribute qa[1];
-          qa[0].id = cudaLaunchAttributeClusterDimension;
-          qa[0].val.clusterDim.x = c;
-          qa[0].val.clusterDim.y = 1;
-          qa[0].val.clusterDim.z = 1;
-          q.attrs = qa;
-          int nc = 0;
-          if (cudaOccupancyMaxActiveClusters(&nc, kern, &q) == cudaSuccess && nc > 0) cl_size = c;
-        }
+  };
+  // slab mode: one cluster (16, else 8 CTAs) when every level is 3D, of one
+  // precision, without DSH rescaling, and the base level is a CTA-0 level
+  static int cl_env = -1;
+  if (cl_env < 0) {
+    const char* e = std::getenv("MPMG_COARSE_CLUSTER");
+    cl_env = e ? std::atoi(e) : 16;
+  }
+  bool slab_ok = cl_env > 1 && UP < 3 && !a.rescale && !small_level(T, a.cta_points) &&
+                 small_level(a.lv[0], a.cta_points);
+  for (int l = 0; l < a.nlev && slab_ok; ++l) slab_ok = a.lv[l].dim == 3 && a.lv[l].nodes - 1 >= 2;
+  if (slab_ok) {
+    static int tried = 0, ok16 = 0, ok8 = 0;
+    if (!tried) {
+      tried = 1;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    for (int c = std::min(cl_env, 16); c >= 8; c /= 2) {
+      const size_t smem = slab_smem(a, c, nullptr, nullptr);
+      if (smem > 200 * 1024) continue;
+      int& ok = c == 16 ? ok16 : ok8;
+      want_smem(smem);
+      if (ok == 0) {  // can a cluster of c CTAs with this footprint be resident?
+        cudaLaunchConfig_t q = cfg;
+        q.gridDim = dim3(c);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = c;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        int nc = 0;
+        ok = (cudaOccupancyMaxActiveClusters(&nc, kern, &q) == cudaSuccess && nc > 0) ? 1 : -1;
         cudaGetLastError();
       }
-      if (cl_size > 1) cluster = cl_size;
-    }
-    if (cluster) {
-      grid = (unsigned)cluster;
+      if (ok < 0) continue;
+      cfg.gridDim = dim3(c);
+      cfg.dynamicSmemBytes = smem;
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = (unsigned)cluster;
+      at[0].val.clusterDim.x = c;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
-    } else {
-      int dev = 0, sms = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
-      static int per_env = -1;  // MPMG_COARSE_PER_SM: CTAs per SM (<= occupancy)
-      if (per_env < 0) {
-        const char* e = std::getenv("MPMG_COARSE_PER_SM");
-        per_env = e ? std::atoi(e) : 0;
-      }
-      if (per_env > 0) per = std::min(per, per_env);
-      grid = (unsigned)std::max(1, per) * (unsigned)std::max(1, sms);
+      return cudaLaunchKernelEx(&cfg, kern, a, 1, c);
     }
   }
-  if (!cluster) {
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+  const size_t smem = coarse_smem(a);
+  const int use_smem = smem <= 200 * 1024 ? 1 : 0;
+  const size_t dyn = use_smem ? smem : 0;
+  if (use_smem) want_smem(smem);
+  // grid: one CTA when every level is a CTA-0 level, else every co-resident
+  // CTA as a cooperative grid
+  unsigned grid = 1;
+  if (!small_level(T, a.cta_points)) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+    static int per_env = -1;  // MPMG_COARSE_PER_SM: CTAs per SM (<= occupancy)
+    if (per_env < 0) {
+      const char* e = std::getenv("MPMG_COARSE_PER_SM");
+      per_env = e ? std::atoi(e) : 0;
+    }
+    if (per_env > 0) per = std::min(per, per_env);
+    grid = (unsigned)std::max(1, per) * (unsigned)std::max(1, sms);
   }
   cfg.gridDim = dim3(grid);
-  return cudaLaunchKernelEx(&cfg, kern, a, use_smem, cluster);
+  cfg.dynamicSmemBytes = dyn;
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, use_smem, 0);
 }
 
 template <bool FTZ, bool FMA, bool ACC32>
