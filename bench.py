@@ -207,7 +207,7 @@ def run_b200(a):
             t = float(tt.item())
         results[tag] = dict(variant=variant, seconds=t, iterations=int(its[-1]), min_s=float(np.min(times)),
                             final_residual=rep.final_residual, graph=bool(graph_used))
-        launches_per_solve[tag] = solve_launches(h, its[-1], a)
+        launches_per_solve[tag] = solve_launches(h, its[-1], a, variant)
         if tag == "mixed":
             # e2e through the public C ABI with pinned HOST buffers: H2D of b,
             # pack, solve, unpack, D2H of u inside the timed region
@@ -291,20 +291,21 @@ def run_b200(a):
         torch.distributed.destroy_process_group()
 
 
-def solve_launches(h, iterations, a):
+def solve_launches(h, iterations, a, variant):
     """Kernels launched by one graph-captured solve (see mpmg_solver.cu):
-    init = state reset + FP64 defect + control; per iteration = downcast +
-    per streaming level (pre + post Jacobi steps, defect, restriction,
-    prolongation) + one coarse-CTA kernel + update_rc + gated refresh defect +
-    control; final = residual-norm defect + finalize."""
-    lib = h  # noqa
-    big = 0
-    for l in range(h.levels):
-        if ((h.level_nodes(l) - 1) >= 64):
-            big += 1
-    per_level = a.pre + a.post + 3
-    per_it = 1 + big * per_level + 1 + 1 + 1 + 1
-    return 3 + iterations * per_it + 2
+    init = state reset + r = b (or the FP64 defect) + control; per iteration =
+    downcast (not for D_MG, whose scale-1 cast is an alias) + per streaming
+    level (pre-smoothing with the first two steps fused, post-smoothing,
+    defect, restriction, prolongation) + one coarse kernel + outer update
+    (+ the gated fold of parked corrections for binary16/32 finest levels) +
+    gated refresh defect + control; final = (fold) + residual-norm defect +
+    finalize."""
+    big = sum(1 for l in range(h.levels) if (h.level_nodes(l) - 1) >= 64)
+    deferred = variant in ("h_mg", "hsd_mg")
+    pre = a.pre - 1 if a.pre >= 2 else a.pre
+    per_level = pre + a.post + 3
+    per_it = (0 if variant == "d_mg" else 1) + big * per_level + 1 + 1 + (1 if deferred else 0) + 1 + 1
+    return 3 + iterations * per_it + (1 if deferred else 0) + 2
 
 
 def load_peaks():
@@ -359,13 +360,25 @@ def kernel_roofline(a, dim, n, L, ftz, dev, flush_l2):
                          r64=padded(torch.float64, mg.FP64), u64=padded(torch.float64, mg.FP64),
                          b64=padded(torch.float64, mg.FP64)))
     alpha = torch.tensor([1e-3], dtype=torch.float64, device=dev)
-    part = torch.zeros(lib.mpmg_gpu_partials_len(dim, n), dtype=torch.float64, device=dev)
+    npart = lib.mpmg_gpu_partials_len(dim, n)
+    if prec != mg.FP64:
+        npart = max(npart, lib.mpmg_gpu_update_r_partials(dim, n, prec))
+    part = torch.zeros(npart, dtype=torch.float64, device=dev)
+    # deferred-correction ring (the solver's binary16 outer update): one slot
+    ring_len = (plen + 63) // 64 * 64
+    ring = torch.zeros(ring_len, dtype=tdt, device=dev)
+    slot = torch.zeros(1, dtype=torch.int32, device=dev)
+    rscale = torch.zeros(1, dtype=torch.float64, device=dev)
     specs = {
         "jacobi_fine": (3 * bp * N, lambda s: lib.mpmg_gpu_jacobi(C.byref(A), s["b"].data_ptr(), s["u"].data_ptr(),
                                                                   s["u2"].data_ptr(), 2.0 / 3.0, pol, sp)),
         "update_rc": ((32 + bp) * N, lambda s: lib.mpmg_gpu_update_rc(C.byref(A64), s["u"].data_ptr(), prec,
                                                                       s["r64"].data_ptr(), s["u64"].data_ptr(),
                                                                       alpha.data_ptr(), part.data_ptr(), pol, sp)),
+        "update_r": ((16 + 2 * bp) * N, lambda s: lib.mpmg_gpu_update_r(C.byref(A64), s["u"].data_ptr(), prec,
+                                                                        s["r64"].data_ptr(), alpha.data_ptr(),
+                                                                        part.data_ptr(), ring.data_ptr(), ring_len,
+                                                                        slot.data_ptr(), rscale.data_ptr(), pol, sp)),
         "downcast": ((8 + bp) * N, lambda s: lib.mpmg_gpu_scale_downcast(dim, n, s["r64"].data_ptr(),
                                                                          s["u2"].data_ptr(), prec, alpha.data_ptr(),
                                                                          1, pol, sp)),
@@ -373,6 +386,8 @@ def kernel_roofline(a, dim, n, L, ftz, dev, flush_l2):
                                                                 s["u64"].data_ptr(), s["r64"].data_ptr(),
                                                                 part.data_ptr(), sp)),
     }
+    if prec == mg.FP64:  # the FP64 finest level keeps the fused update
+        specs.pop("update_r")
     res = {}
     reps = max(a.kernel_reps, nsets)
     for name, (nbytes, fn) in specs.items():
@@ -390,8 +405,11 @@ def kernel_roofline(a, dim, n, L, ftz, dev, flush_l2):
                      "timing": f"{reps} launches rotating over {nsets} buffer sets (operands evicted from L2)"}
     # per iteration: the finest Jacobi kernel runs pre + post - 2 times (the
     # first two pre-smoothing steps are one fused JACOBI_Z pass)
+    # the outer update the solve runs: r-only + ring for binary16/32 finest
+    # levels (u folded once per refresh), the fused update for FP64
+    upd = "update_r" if "update_r" in res else "update_rc"
     share = {"jacobi_fine": res["jacobi_fine"]["avg_us"] * max(1, a.pre + a.post - 2),
-             "update_rc": res["update_rc"]["avg_us"], "downcast": res["downcast"]["avg_us"],
+             upd: res[upd]["avg_us"], "downcast": res["downcast"]["avg_us"],
              "defect64": res["defect64"]["avg_us"] / 10.0}
     res["dominant"] = max(share, key=share.get)
     for k in share:

@@ -142,6 +142,22 @@ int mpmg_gpu_defect_f64(const mpmg_stencil* A64, const double* b, const double* 
 int mpmg_gpu_update_rc(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, double* u,
                        const double* alpha_dev, double* partials, uint32_t policy, void* stream);
 
+/* Deferred-correction halves of update_residuum_correction (kernels.cpp:
+ * 300-341), as the solver runs them for binary16/32 finest levels:
+ * update_r: r_i = fma(-alpha, (A c)_i, r_i) (+ partial sums of r_i^2 as in
+ *   update_rc) and c copied into ring slot *slot_dev (ring_len values per
+ *   slot, ring_len * bytes a multiple of 64), ring_scale[*slot_dev] = alpha.
+ *   3D levels with pitch 32..1024 only (MPMG_EUNSUPPORTED otherwise).
+ * fold: u_i = fma(ring_scale[k], c_k,i, u_i) for k = 0 .. *count_dev - 1 in
+ *   order -- bitwise the u half of the per-iteration update. len = padded
+ *   length of u. */
+int mpmg_gpu_update_r(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, const double* alpha_dev,
+                      double* partials, void* ring, int64_t ring_len, const int32_t* slot_dev, double* ring_scale,
+                      uint32_t policy, void* stream);
+int mpmg_gpu_update_r_partials(int32_t dim, int32_t nodes, int32_t c_prec);
+int mpmg_gpu_fold(int64_t len, double* u, const void* ring, int64_t ring_len, int32_t c_prec,
+                  const double* ring_scale, const int32_t* count_dev, uint32_t policy, void* stream);
+
 /* Scaled downcast (cast_vector kernels.cpp:343-360): out = round_prec(x / s)
  * with s = *alpha_dev if (scale_enabled && *alpha_dev > 0) else 1. */
 int mpmg_gpu_scale_downcast(int32_t dim, int32_t nodes, const double* x, void* out, int32_t prec,

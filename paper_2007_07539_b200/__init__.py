@@ -136,6 +136,10 @@ def lib():
     L.mpmg_gpu_prolong_correct.argtypes = [i32, i32, i32, i32, vp, vp, vp, u32, vp]
     L.mpmg_gpu_defect_f64.restype = i; L.mpmg_gpu_defect_f64.argtypes = [sp, vp, vp, vp, vp, vp]
     L.mpmg_gpu_update_rc.restype = i; L.mpmg_gpu_update_rc.argtypes = [sp, vp, i32, vp, vp, vp, vp, u32, vp]
+    L.mpmg_gpu_update_r.restype = i
+    L.mpmg_gpu_update_r.argtypes = [sp, vp, i32, vp, vp, vp, vp, C.c_int64, vp, vp, u32, vp]
+    L.mpmg_gpu_update_r_partials.restype = i; L.mpmg_gpu_update_r_partials.argtypes = [i32, i32, i32]
+    L.mpmg_gpu_fold.restype = i; L.mpmg_gpu_fold.argtypes = [C.c_int64, vp, vp, C.c_int64, i32, vp, vp, u32, vp]
     L.mpmg_gpu_scale_downcast.restype = i
     L.mpmg_gpu_scale_downcast.argtypes = [i32, i32, vp, vp, i32, vp, i32, u32, vp]
     L.mpmg_gpu_partials_len.restype = i; L.mpmg_gpu_partials_len.argtypes = [i32, i32]

@@ -90,6 +90,31 @@ int mpmg_gpu_update_rc(const mpmg_stencil* A64, const void* c, int32_t c_prec, d
   return rc(launch_update_rc(*A64, c, c_prec, r, u, alpha_dev, partials, policy & MPMG_FMA, (cudaStream_t)stream));
 }
 
+int mpmg_gpu_update_r(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, const double* alpha_dev,
+                      double* partials, void* ring, int64_t ring_len, const int32_t* slot_dev, double* ring_scale,
+                      uint32_t policy, void* stream) {
+  if (!valid_stencil(A64) || A64->prec != MPMG_FP64 || !c || !valid_prec(c_prec) || !r || !alpha_dev || !ring ||
+      ring_len < (int64_t)mpmg_padded_len(A64->dim, A64->nodes) || !slot_dev || !ring_scale)
+    return MPMG_EINVAL;
+  cudaError_t e = cudaSuccess;
+  if (!plane_update_r(*A64, c, c_prec, r, alpha_dev, partials, ring, (long long)ring_len, slot_dev, ring_scale,
+                      policy & MPMG_FMA, (cudaStream_t)stream, &e))
+    return MPMG_EUNSUPPORTED;
+  return rc(e);
+}
+
+int mpmg_gpu_update_r_partials(int32_t dim, int32_t nodes, int32_t c_prec) {
+  const int n = plane_update_r_partials(dim, nodes, c_prec);
+  return n > 0 ? n : MPMG_EUNSUPPORTED;
+}
+
+int mpmg_gpu_fold(int64_t len, double* u, const void* ring, int64_t ring_len, int32_t c_prec,
+                  const double* ring_scale, const int32_t* count_dev, uint32_t policy, void* stream) {
+  if (len < 1 || !u || !ring || ring_len < len || !valid_prec(c_prec) || !ring_scale || !count_dev) return MPMG_EINVAL;
+  return rc(launch_fold((size_t)len, u, ring, (long long)ring_len, c_prec, ring_scale, count_dev, 0, nullptr,
+                        policy & MPMG_FMA, (cudaStream_t)stream));
+}
+
 int mpmg_gpu_scale_downcast(int32_t dim, int32_t nodes, const double* x, void* out, int32_t prec,
                             const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream) {
   if ((dim != 2 && dim != 3) || nodes < 3 || !x || !out || !valid_prec(prec) || !alpha_dev) return MPMG_EINVAL;

@@ -133,11 +133,14 @@ struct Lv {
   static __device__ __forceinline__ T apply(const Taps& k, int dim, const T* x, int i, int P) {
     return dim == 3 ? apply_d<3>(k, x, i, P) : apply_d<2>(k, x, i, P);
   }
-  // A x on a one-unknown level: every neighbour is a (zero) ghost. The same
-  // operation sequence as apply(), on a register value.
+  // A x on a one-unknown level: every neighbour is a (zero) ghost, so
+  // apply()'s chain is +0 until the centre tap and unchanged after it (the
+  // taps are finite: fma(t, +0, acc) = acc + (+-0) = acc for acc != 0, and
+  // acc = +0 stays +0) -- bitwise the centre term alone, on a register.
   static __device__ __forceinline__ T apply1(const Taps& k, int dim, T x) {
-    auto ld = [&](int dz, int dy, int dx) { return (dz | dy | dx) == 0 ? x : zero(); };
-    return dim == 3 ? apply_f<3>(k, ld) : apply_f<2>(k, ld);
+    const int c = dim == 3 ? 13 : 4;
+    if constexpr (PR == P16 && ACC32) return f16s<FTZ>(__float2half_rn(fma32<FTZ, FMA>(k.f[c], __half2float(x), 0.0f)));
+    else return fma(k.t[c], x, zero());
   }
 };
 
@@ -184,7 +187,9 @@ __host__ __device__ inline int slab_lo(int P_top, int C, int shift, int r) {
   return (lt + (1 << shift) - 1) >> shift;
 }
 // elements of one slab buffer of a level with pitch P and at most nz owned planes
-__host__ __device__ inline long long slab_elems(int P, int nz) { return (long long)(nz + 3) * P * P; }
+// (halo planes included; the top halo plane's aliased x = P / y = P ghosts
+// reach P + 1 values past it)
+__host__ __device__ inline long long slab_elems(int P, int nz) { return (long long)(nz + 2) * P * P + P + 1; }
 __host__ __device__ inline int slab_max_nz(int P_top, int C, int shift) {
   int m = 0;
   for (int r = 0; r < C; ++r) {
@@ -318,8 +323,64 @@ struct Coarse {
     }
   }
 
+  // binary16 slab levels (3D): two x-neighbours per thread in one half2 --
+  // three aligned 32-bit loads per stencil row, the x-1 / x+1 pairs by byte
+  // permutes, HFMA2 on both nodes in the slot order of apply() (each lane is
+  // the scalar chain, bitwise). DEF: defect r = b - A u, else a Jacobi step.
+  // The pair (0, 1) computes the x = 0 ghost and stores it as zero.
+  template <bool DEF>
+  __device__ void pairs16(const CoarseLevel& L, const void* bv, const void* uv, void* ov, bool from_zero) {
+    using OP = O<P16>;
+    const int l = (int)(&L - lv);
+    const int P = L.nodes - 1, P2 = P * P, hp = P / 2;
+    const int zlo = lo(l, (int)rank), nz = lo(l, (int)rank + 1) - zlo;
+    const int np = (P - 1) * hp;  // pairs per plane
+    const __half* u = static_cast<const __half*>(uv);
+    const __half* b = static_cast<const __half*>(bv);
+    __half* o = static_cast<__half*>(ov);
+    const auto tk = taps_of<P16>(L);
+    __half2 t2[27];
+#pragma unroll
+    for (int t = 0; t < 27; ++t) t2[t] = __half2half2(tk.t[t]);
+    const __half2 m1 = u2h(0xBC00BC00u);
+    const __half2 w = __half2half2(OP::from(L.omega)), d = __half2half2(OP::from(L.inv_diag));
+    const __half2 z2 = u2h(0u);
+    for (int k = threadIdx.x; k < np * nz; k += blockDim.x) {
+      const int zq = k / np, rem = k - zq * np;
+      const int y = 1 + rem / hp, x = 2 * (rem - (y - 1) * hp);
+      const int i = (zlo + zq) * P2 + y * P + x;
+      __half2 acc = z2, uc = z2;
+      if (DEF || !from_zero) {
+        int t = 0;
+#pragma unroll
+        for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+          for (int dy = -1; dy <= 1; ++dy, t += 3) {
+            const uint32_t* row = reinterpret_cast<const uint32_t*>(u + i + dz * P2 + dy * P);
+            const uint32_t w0 = row[-1], w1 = row[0], w2 = row[1];
+            const __half2 lft = u2h(__byte_perm(w0, w1, 0x5432)), rgt = u2h(__byte_perm(w1, w2, 0x5432));
+            acc = fma16<FTZ, FMA>(t2[t], lft, acc);
+            acc = fma16<FTZ, FMA>(t2[t + 1], u2h(w1), acc);
+            acc = fma16<FTZ, FMA>(t2[t + 2], rgt, acc);
+            if (dz == 0 && dy == 0) uc = u2h(w1);
+          }
+      }
+      const __half2 bb = u2h(*reinterpret_cast<const uint32_t*>(b + i));
+      const __half2 r = fma16<FTZ, FMA>(m1, acc, bb);
+      __half2 out = DEF ? r : fma16<FTZ, FMA>(w, mul16<FTZ>(d, r), uc);
+      if (x == 0) out = u2h(h2u(out) & 0xFFFF0000u);  // ghost node stays +0
+      *reinterpret_cast<uint32_t*>(o + i) = h2u(out);
+    }
+  }
+  __device__ bool pairs_ok(const CoarseLevel& L) const {
+    return slab && !small(L) && L.dim == 3 && ((L.nodes - 1) & 1) == 0;
+  }
+
   template <int PR>
   __device__ void jacobi(const CoarseLevel& L, const void* bv, const void* uin, void* uout, bool from_zero) {
+    if constexpr (PR == P16 && !ACC32) {
+      if (pairs_ok(L)) { pairs16<false>(L, bv, uin, uout, from_zero); return; }
+    }
     using OP = O<PR>;
     using T = typename OP::T;
     const T* b = static_cast<const T*>(bv);
@@ -336,6 +397,9 @@ struct Coarse {
 
   template <int PR>
   __device__ void defect(const CoarseLevel& L, const void* bv, const void* uv, void* rv) {
+    if constexpr (PR == P16 && !ACC32) {
+      if (pairs_ok(L)) { pairs16<true>(L, bv, uv, rv, false); return; }
+    }
     using OP = O<PR>;
     using T = typename OP::T;
     const T m1 = OP::from(-1.0);
@@ -948,7 +1012,7 @@ cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
     }
     for (int c = std::min(cl_env, 16); c >= 8; c /= 2) {
       const size_t smem = slab_smem(a, c, nullptr, nullptr);
-      if (smem > 200 * 1024) continue;
+      if (smem > 212 * 1024) continue;  // + ~10 KB of static tables <= 227 KB per CTA
       int& ok = c == 16 ? ok16 : ok8;
       want_smem(smem);
       if (ok == 0) {  // can a cluster of c CTAs with this footprint be resident?

@@ -83,3 +83,52 @@ def test_generic_ell_spmv(prec, ftz, fma, acc32):
     torch.cuda.synchronize()
     ref = O.spmv(cols, vals, prec, x, O.ctx(ftz, fma, acc32))
     assert same(yd.double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("fma", [True, False])
+def test_update_r_and_fold_equal_fused_update(fma):
+    """mpmg_gpu_update_r (r half + ring slot) followed by mpmg_gpu_fold (u half)
+    equals the fused mpmg_gpu_update_rc (kernels.cpp:300-341) bitwise, over two
+    iterations with different scales."""
+    import torch
+    L = mg.lib()
+    dim, n = 3, 65
+    plen = L.mpmg_padded_len(dim, n)
+    pol = mg.policy_word(False, fma, False)
+    A64 = mg.level_stencil(dim, n, mg.FP64, False)
+    rng = np.random.default_rng(5)
+
+    def padded(prec, scale):
+        comp = (rng.random(mg.unknowns(dim, n)) * 2 - 1) * scale
+        comp = O.round_vec(comp, prec, False)
+        out = torch.zeros(plen, dtype=torch.float16 if prec == FP16 else torch.float64, device="cuda")
+        src = torch.from_numpy(comp.astype(np.float16 if prec == FP16 else np.float64)).cuda()
+        mg._check(L.mpmg_gpu_pack(dim, n, prec, src.data_ptr(), out.data_ptr(), None), "pack")
+        return out
+
+    r0, u0 = padded(FP64, 1.0), padded(FP64, 1.0)
+    cs = [padded(FP16, 1.0), padded(FP16, 1e-3)]
+    alphas = [dev(np.array([0.37])), dev(np.array([2.5e-4]))]
+    npart = L.mpmg_gpu_partials_len(dim, n)
+    p1 = torch.zeros(npart, dtype=torch.float64, device="cuda")
+    r1, u1 = r0.clone(), u0.clone()
+    for c, a in zip(cs, alphas):
+        assert L.mpmg_gpu_update_rc(C.byref(A64), c.data_ptr(), FP16, r1.data_ptr(), u1.data_ptr(), a.data_ptr(),
+                                    p1.data_ptr(), pol, None) == 0
+    ring_len = (plen + 63) // 64 * 64
+    ring = torch.zeros(2 * ring_len, dtype=torch.float16, device="cuda")
+    scales = torch.zeros(2, dtype=torch.float64, device="cuda")
+    assert L.mpmg_gpu_update_r_partials(dim, n, FP16) > 0
+    p2 = torch.zeros(max(npart, L.mpmg_gpu_update_r_partials(dim, n, FP16)), dtype=torch.float64, device="cuda")
+    r2, u2 = r0.clone(), u0.clone()
+    for k, (c, a) in enumerate(zip(cs, alphas)):
+        slot = torch.tensor([k], dtype=torch.int32, device="cuda")
+        assert L.mpmg_gpu_update_r(C.byref(A64), c.data_ptr(), FP16, r2.data_ptr(), a.data_ptr(), p2.data_ptr(),
+                                   ring.data_ptr(), ring_len, slot.data_ptr(), scales.data_ptr(), pol, None) == 0
+    cnt = torch.tensor([2], dtype=torch.int32, device="cuda")
+    assert L.mpmg_gpu_fold(plen, u2.data_ptr(), ring.data_ptr(), ring_len, FP16, scales.data_ptr(), cnt.data_ptr(),
+                           pol, None) == 0
+    torch.cuda.synchronize()
+    assert same(r1.cpu().numpy().view(np.uint64), r2.cpu().numpy().view(np.uint64))
+    assert same(u1.cpu().numpy().view(np.uint64), u2.cpu().numpy().view(np.uint64))
+    assert same(scales.cpu().numpy(), np.array([0.37, 2.5e-4]))
