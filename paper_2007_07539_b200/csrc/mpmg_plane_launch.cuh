@@ -51,6 +51,17 @@ inline int outer_waves() {
   return v;
 }
 
+// minimum output planes per CTA below pitch 256 (MPMG_ZMIN_SMALL, tuning)
+inline int small_zmin() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_ZMIN_SMALL");
+    v = e ? std::atoi(e) : 1;
+    if (v < 1 || v > 64) v = 1;
+  }
+  return v;
+}
+
 inline __half2 h2_of(double v) {
   const __half h = __double2half(v);
   return __halves2half2(h, h);
@@ -107,7 +118,7 @@ struct PlaneLaunch {
     int z = (pz - 1 + chunks - 1) / chunks;
     // small grids are latency-bound: as many CTAs as possible; large grids
     // keep >= 2 planes per chunk so the z-halo re-reads stay small
-    const int zmin = P >= 256 ? 2 : 1;
+    const int zmin = P >= 256 ? 2 : small_zmin();
     if (z < zmin) z = zmin;
     *zc = z;
     return dim3(ytiles, (pz - 1 + z - 1) / z, 1);
