@@ -778,4 +778,97 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
   }
 }
 
+// ---- direct-load variant for small L2-resident levels ---------------------
+// One warp per output row (x width P = 32 W), no shared-memory staging: each
+// lane loads its W values of the 9 neighbour rows straight from L2 and shifts
+// them like k_plane (WX = 1). Same per-output slot order and epilogue as
+// k_plane, so the results are bitwise those of the plane kernel; it trades
+// 9x L2 reads for no pipeline fill, which wins on the latency-bound levels.
+template <int LP, int OP, bool FTZ, bool FMA, bool SKIPF, int W>
+__global__ void __launch_bounds__(128) k_direct(const __grid_constant__ PlaneArgs a) {
+  using ST = typename Sc<LP>::T;
+  constexpr int P = 32 * W;
+  constexpr bool kJZ = OP == POP_JACOBI_Z;
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31;
+  const int rr = (int)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (rr >= (P - 1) * (P - 1)) return;  // warp-uniform
+  const int y = 1 + rr % (P - 1), z = 1 + rr / (P - 1);
+  const int x0 = lane * W;
+  const long long plane = (long long)P * P;
+  uint32_t tk[27];
+  if constexpr (LP == P16) {
+#pragma unroll
+    for (int k = 0; k < 27; ++k) tk[k] = (SKIPF && is_face(k)) ? 0u : h2u(a.t16[k]);
+  }
+  auto tapk = [&](int k) {
+    if constexpr (LP == P16) return u2h(tk[k]);
+    else return tap<LP>(a, k);
+  };
+  const auto jd = [&] {
+    if constexpr (LP == P16) return a.d16;
+    else if constexpr (LP == P32) return a.d32;
+    else return a.d64;
+  }();
+  const auto jw = [&] {
+    if constexpr (LP == P16) return a.w16;
+    else if constexpr (LP == P32) return a.w32;
+    else return a.w64;
+  }();
+  (void)jd; (void)jw;
+  const long long gi = z * plane + (long long)y * P + x0;
+  Row<LP, W> acc, ctr;
+  rzero(acc);
+  rzero(ctr);
+#pragma unroll
+  for (int tz = 0; tz < 3; ++tz)
+#pragma unroll
+    for (int ty = 0; ty < 3; ++ty) {
+      Row<LP, W> c, L, R;
+      gload<LP, W>(a.x, gi + (tz - 1) * plane + (ty - 1) * P, c);
+      if constexpr (kJZ) jz_row<LP, FTZ, FMA, W>(jd, jw, c);
+      if (tz == 1 && ty == 1) ctr = c;
+      ST prev = shup(rlast<LP, W>(c));
+      ST next = shdn(rfirst<LP, W>(c));
+      if (lane == 0) prev = ST(0);   // x = -1: only feeds the ghost output x = 0
+      if (lane == 31) next = ST(0);  // x = P: the aliased ghost (zero)
+      rshift<LP, W>(c, prev, next, L, R);
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int k = tz * 9 + ty * 3 + dx;
+        if (SKIPF && is_face(k)) continue;
+        rfma<LP, FTZ, FMA, W>(tapk(k), dx == 0 ? L : (dx == 1 ? c : R), acc);
+      }
+    }
+  Row<LP, W> bb;
+  if constexpr (kJZ) gload<LP, W>(a.x, gi, bb);  // operand == b
+  else gload<LP, W>(a.b, gi, bb);
+  if constexpr (LP == P16) {
+    const __half2 m1 = u2h(0xBC00BC00u);
+    Row<LP, W> r = efma<LP, FTZ, FMA, W>(m1, acc, bb);
+    if constexpr (OP == POP_DEFECT) {
+      if (x0 == 0) rzero_first<LP, W>(r);
+      gstore<LP, W>(a.out, gi, r);
+    } else {
+      const Row<LP, W> dr = emul<LP, FTZ, W>(a.d16, r);
+      Row<LP, W> un = efma<LP, FTZ, FMA, W>(a.w16, dr, ctr);  // ctr: u, or u1 = w D^-1 b (JACOBI_Z)
+      if (x0 == 0) rzero_first<LP, W>(un);
+      gstore<LP, W>(a.out, gi, un);
+    }
+  } else {
+    const ST m1 = ST(-1), dd = LP == P32 ? (ST)a.d32 : (ST)a.d64, ww = LP == P32 ? (ST)a.w32 : (ST)a.w64;
+    Row<LP, W> r = efma<LP, FTZ, FMA, W>(m1, acc, bb);
+    if constexpr (OP == POP_DEFECT) {
+      if (x0 == 0) rzero_first<LP, W>(r);
+      gstore<LP, W>(a.out, gi, r);
+    } else {
+      const Row<LP, W> dr = emul<LP, FTZ, W>(dd, r);
+      Row<LP, W> un = efma<LP, FTZ, FMA, W>(ww, dr, ctr);
+      if (x0 == 0) rzero_first<LP, W>(un);
+      gstore<LP, W>(a.out, gi, un);
+    }
+  }
+}
+
 }  // namespace mpmg_dev

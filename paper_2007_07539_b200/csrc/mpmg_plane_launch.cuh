@@ -51,6 +51,28 @@ inline int outer_waves() {
   return v;
 }
 
+// largest pitch run by the direct-load kernel (MPMG_DIRECT_MAX_P; measured:
+// 3.65 vs 4.2 us per Jacobi step at 65^3, slower than k_plane from 129^3 up)
+inline int direct_max_pitch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_DIRECT_MAX_P");
+    v = e ? std::atoi(e) : 64;
+  }
+  return v;
+}
+
+// smallest pitch the plane kernels take level ops for (MPMG_PLANE_MIN_P,
+// tuning; below it the streaming stencil kernels run)
+inline int plane_min_pitch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_PLANE_MIN_P");
+    v = e ? std::atoi(e) : 0;
+  }
+  return v;
+}
+
 // minimum output planes per CTA below pitch 256 (MPMG_ZMIN_SMALL, tuning)
 inline int small_zmin() {
   static int v = -1;
@@ -169,6 +191,7 @@ template <int LP>
 bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                     uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr) {
   if (A.dim != 3 || (op != 1 && op != 2 && op != 3)) return false;
+  if (pitch(A.nodes) < plane_min_pitch()) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
   if (LP == P16 && !faces_zero16(A)) return false;
   if (!aligned16(x) || !aligned16(b) || !aligned16(out)) return false;
@@ -179,6 +202,19 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
   a.w16 = h2_of(w); a.w32 = (float)w; a.w64 = w;
   return with_pitch(a.P, [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
+    if constexpr (PP <= 256) {
+      if (!slab && PP <= direct_max_pitch()) {  // small L2-resident level: direct loads
+        constexpr int W = PP / 32;
+        constexpr bool SK = LP == P16;
+        const dim3 g((unsigned)(((PP - 1) * (PP - 1) + 3) / 4));
+        auto go = [&](auto kern) { *err = launch_pdl(kern, g, dim3(128), 0, s, a); };
+        if (op == 1) ftz ? go(k_direct<LP, POP_DEFECT, true, true, SK, W>) : go(k_direct<LP, POP_DEFECT, false, true, SK, W>);
+        else if (op == 3) ftz ? go(k_direct<LP, POP_JACOBI_Z, true, true, SK, W>)
+                              : go(k_direct<LP, POP_JACOBI_Z, false, true, SK, W>);
+        else ftz ? go(k_direct<LP, POP_JACOBI, true, true, SK, W>) : go(k_direct<LP, POP_JACOBI, false, true, SK, W>);
+        return;
+      }
+    }
     if (op == 1) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_DEFECT, true, true, PP>::run(a, s)
                             : PlaneLaunch<LP, LP, LP, POP_DEFECT, false, true, PP>::run(a, s);
     else if (op == 3) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, true, true, PP>::run(a, s)
