@@ -18,7 +18,7 @@ using namespace mpmg_dev;
 // Jacobi only)
 template <int LP, int CP, int OP, int P, int V = 0>
 struct PlaneCfg {
-  static constexpr int W = P >= 256 ? 8 : P / 32;
+  static constexpr int W = (V == 10 && P >= 128) ? 4 : (P >= 256 ? 8 : P / 32);
   static constexpr int WX = P / (32 * W);
   static constexpr bool kWide = CP == P64 || (CP == P32 && LP != P16) || OP == POP_UPDATE || OP == POP_UPDATE_R;
   // output rows per thread and warp-rows per CTA
@@ -27,7 +27,7 @@ struct PlaneCfg {
   static constexpr int NS0 = kWide && W == 8 ? 3 : 4;
   static constexpr int RY = V == 1 ? 2 : (V == 2 ? 2 : (V == 3 ? 4 : (V == 5 ? 1 : RY0)));
   static constexpr int WY = V == 2 ? 8 : (V == 3 ? 2 : (V == 5 ? 8 : WY0));
-  static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : NS0);
+  static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : (V == 10 ? 4 : NS0));
   static constexpr int OPT = V == 4 ? 1 : 0;
 };
 

@@ -4,6 +4,8 @@
 // precision (kernels.cpp:300-341).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "mpmg_plane_launch.cuh"
 
 namespace mpmg_impl {
@@ -19,6 +21,22 @@ int plane_num_sms() {
   return n;
 }
 
+// CTA shape of the FP64 outer updates: 4 values per lane, two warps per
+// 256-wide row (PlaneCfg V = 10) -- fewer registers per thread and more CTAs
+// than 8 values per lane (UPDATE_R 73.6 -> 69.9 us at 257^3; the D_MG solve
+// with the fused UPDATE 7.66 -> 7.28 ms)
+constexpr int OV = 10;
+// DEFECT64 / RESNORM shape (MPMG_DEF64_SHAPE: 0 = 8 values per lane, the
+// default -- 84 vs 91 us at 257^3 --, else OV)
+static int def_shape() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_DEF64_SHAPE");
+    v = e ? std::atoi(e) : 0;
+  }
+  return v;
+}
+
 bool plane_outer_supported(int dim, int nodes) {
   if (dim != 3) return false;
   return with_pitch(pitch(nodes), [](auto) {});
@@ -31,9 +49,15 @@ bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, d
   a.x = u; a.b = b; a.out = r; a.partials = partials; a.gate = gate;
   return with_pitch(a.P, [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
-    if (resnorm) *err = PlaneLaunch<P64, P64, P64, POP_RESNORM, false, true, PP>::run(a, s);  // ir_solver.cpp:38
-    else if (fma) *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::run(a, s);
-    else *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, false, PP>::run(a, s);
+    if (def_shape() == 0) {
+      if (resnorm) *err = PlaneLaunch<P64, P64, P64, POP_RESNORM, false, true, PP>::run(a, s);
+      else if (fma) *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::run(a, s);
+      else *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, false, PP>::run(a, s);
+      return;
+    }
+    if (resnorm) *err = PlaneLaunch<P64, P64, P64, POP_RESNORM, false, true, PP, OV>::run(a, s);  // ir_solver.cpp:38
+    else if (fma) *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP, OV>::run(a, s);
+    else *err = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, false, PP, OV>::run(a, s);
   });
 }
 
@@ -47,8 +71,8 @@ bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double*
     constexpr int PP = decltype(pc)::value;
     auto go = [&](auto lpc) {
       constexpr int L = decltype(lpc)::value;
-      *err = fma ? PlaneLaunch<L, P64, P64, POP_UPDATE, false, true, PP>::run(a, s)
-                 : PlaneLaunch<L, P64, P64, POP_UPDATE, false, false, PP>::run(a, s);
+      *err = fma ? PlaneLaunch<L, P64, P64, POP_UPDATE, false, true, PP, OV>::run(a, s)
+                 : PlaneLaunch<L, P64, P64, POP_UPDATE, false, false, PP, OV>::run(a, s);
     };
     switch (c_prec) {
       case MPMG_FP16: go(std::integral_constant<int, P16>{}); break;
@@ -73,8 +97,8 @@ bool plane_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* 
     constexpr int PP = decltype(pc)::value;
     auto go = [&](auto lpc) {
       constexpr int L = decltype(lpc)::value;
-      *err = fma ? PlaneLaunch<L, P64, P64, POP_UPDATE_R, false, true, PP>::run(a, s)
-                 : PlaneLaunch<L, P64, P64, POP_UPDATE_R, false, false, PP>::run(a, s);
+      *err = fma ? PlaneLaunch<L, P64, P64, POP_UPDATE_R, false, true, PP, OV>::run(a, s)
+                 : PlaneLaunch<L, P64, P64, POP_UPDATE_R, false, false, PP, OV>::run(a, s);
     };
     if (c_prec == MPMG_FP16) go(std::integral_constant<int, P16>{});
     else go(std::integral_constant<int, P32>{});
@@ -86,8 +110,8 @@ int plane_update_r_partials(int dim, int nodes, int lp) {
   int n = -1;
   with_pitch(pitch(nodes), [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
-    n = lp == MPMG_FP16 ? PlaneLaunch<P16, P64, P64, POP_UPDATE_R, false, true, PP>::partials()
-                        : PlaneLaunch<P32, P64, P64, POP_UPDATE_R, false, true, PP>::partials();
+    n = lp == MPMG_FP16 ? PlaneLaunch<P16, P64, P64, POP_UPDATE_R, false, true, PP, OV>::partials()
+                        : PlaneLaunch<P32, P64, P64, POP_UPDATE_R, false, true, PP, OV>::partials();
   });
   return n;
 }
@@ -102,11 +126,15 @@ int plane_partials(int dim, int nodes, int lp, bool update, int pz) {
   if (pz <= 0) pz = pitch(nodes);
   with_pitch(pitch(nodes), [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
-    if (!update) { n = PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::partials(pz); return; }
+    if (!update) {
+      n = def_shape() == 0 ? PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP>::partials(pz)
+                           : PlaneLaunch<P64, P64, P64, POP_DEFECT64, false, true, PP, OV>::partials(pz);
+      return;
+    }
     switch (lp) {
-      case MPMG_FP16: n = PlaneLaunch<P16, P64, P64, POP_UPDATE, false, true, PP>::partials(pz); break;
-      case MPMG_FP32: n = PlaneLaunch<P32, P64, P64, POP_UPDATE, false, true, PP>::partials(pz); break;
-      default: n = PlaneLaunch<P64, P64, P64, POP_UPDATE, false, true, PP>::partials(pz); break;
+      case MPMG_FP16: n = PlaneLaunch<P16, P64, P64, POP_UPDATE, false, true, PP, OV>::partials(pz); break;
+      case MPMG_FP32: n = PlaneLaunch<P32, P64, P64, POP_UPDATE, false, true, PP, OV>::partials(pz); break;
+      default: n = PlaneLaunch<P64, P64, P64, POP_UPDATE, false, true, PP, OV>::partials(pz); break;
     }
   });
   return n;
