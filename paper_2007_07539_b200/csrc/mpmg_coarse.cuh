@@ -1080,8 +1080,10 @@ cudaError_t launch_t(const CoarseArgs& a, cudaStream_t s) {
 
 }  // namespace coarse_detail
 
-// one translation unit per FTZ policy (mpmg_coarse_ftz0.cu / _ftz1.cu)
-cudaError_t launch_coarse_ftz0(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
-cudaError_t launch_coarse_ftz1(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
+// one translation unit per policy (mpmg_coarse_f<ftz>m<fma>a<acc32>.cu)
+#define MPMG_COARSE_DECL(F, M, A) cudaError_t launch_coarse_f##F##m##M##a##A(const CoarseArgs& a, cudaStream_t s);
+MPMG_COARSE_DECL(0, 0, 0) MPMG_COARSE_DECL(0, 0, 1) MPMG_COARSE_DECL(0, 1, 0) MPMG_COARSE_DECL(0, 1, 1)
+MPMG_COARSE_DECL(1, 0, 0) MPMG_COARSE_DECL(1, 0, 1) MPMG_COARSE_DECL(1, 1, 0) MPMG_COARSE_DECL(1, 1, 1)
+#undef MPMG_COARSE_DECL
 
 }  // namespace mpmg_impl
