@@ -147,6 +147,15 @@ struct Lv {
 struct Pt {
   int n, m, P, dim;
   unsigned magic;  // ceil(2^32 / m): k / m == umulhi(k, magic) for k < 2^32 / m
+  // compact k -> interior coordinates (1-based; z = 0 in 2D)
+  __device__ __forceinline__ void xyz(int k, int& x, int& y, int& z) const {
+    const unsigned q = __umulhi((unsigned)k, magic);
+    x = k - (int)q * m + 1;
+    if (dim == 2) { y = (int)q + 1; z = 0; return; }
+    const unsigned zz = __umulhi(q, magic);
+    y = (int)(q - zz * m) + 1;
+    z = (int)zz + 1;
+  }
   __device__ __forceinline__ int idx(int k) const {  // compact k -> padded index
     const unsigned q = __umulhi((unsigned)k, magic);
     const int x = k - (int)q * m + 1;
@@ -265,6 +274,24 @@ struct Coarse {
   }
   // mode 0: each CTA walks every point; 1: the points are spread over the
   // grid; 2 (slab mode): this CTA's planes
+  // as for_points_by, with the point's coordinates: f(i, x, y, z, P)
+  template <typename F>
+  __device__ void for_points_xyz(const CoarseLevel& L, int mode, F&& f) {
+    const Pt p = points(L);
+    int start = threadIdx.x, stride = blockDim.x, end = p.n;
+    if (mode == 1) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
+    if (mode == 2) {
+      const int l = (int)(&L - lv);
+      const int m2 = p.m * p.m;
+      start += (lo(l, (int)rank) - 1) * m2;
+      end = (lo(l, (int)rank + 1) - 1) * m2;
+    }
+    for (int k = start; k < end; k += stride) {
+      int x, y, z;
+      p.xyz(k, x, y, z);
+      f((z * p.P + y) * p.P + x, x, y, z, p.P);
+    }
+  }
   template <typename F>
   __device__ void for_points_by(const CoarseLevel& L, int mode, F&& f) {
     const Pt p = points(L);
@@ -335,41 +362,54 @@ struct Coarse {
     const int P = L.nodes - 1, P2 = P * P, hp = P / 2;
     const int zlo = lo(l, (int)rank), nz = lo(l, (int)rank + 1) - zlo;
     const int np = (P - 1) * hp;  // pairs per plane
-    const __half* u = static_cast<const __half*>(uv);
-    const __half* b = static_cast<const __half*>(bv);
-    __half* o = static_cast<__half*>(ov);
+    // 32-bit shared-window addresses of the virtual bases (global plane z at
+    // base + 2 z P^2; modular arithmetic, only in-slab addresses are formed)
+    const uint32_t su = (uint32_t)__cvta_generic_to_shared(static_cast<const __half*>(uv) + (long long)(zlo - 1) * P2) -
+                        (uint32_t)((zlo - 1) * P2 * 2);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(static_cast<const __half*>(bv) + (long long)(zlo - 1) * P2) -
+                        (uint32_t)((zlo - 1) * P2 * 2);
+    const uint32_t so = (uint32_t)__cvta_generic_to_shared(static_cast<__half*>(ov) + (long long)(zlo - 1) * P2) -
+                        (uint32_t)((zlo - 1) * P2 * 2);
     const auto tk = taps_of<P16>(L);
     __half2 t2[27];
 #pragma unroll
     for (int t = 0; t < 27; ++t) t2[t] = __half2half2(tk.t[t]);
+    int roff[9];  // byte offsets of the 9 stencil rows
+#pragma unroll
+    for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy) roff[(dz + 1) * 3 + dy + 1] = 2 * (dz * P2 + dy * P);
     const __half2 m1 = u2h(0xBC00BC00u);
     const __half2 w = __half2half2(OP::from(L.omega)), d = __half2half2(OP::from(L.inv_diag));
     const __half2 z2 = u2h(0u);
-    for (int k = threadIdx.x; k < np * nz; k += blockDim.x) {
-      const int zq = k / np, rem = k - zq * np;
-      const int y = 1 + rem / hp, x = 2 * (rem - (y - 1) * hp);
-      const int i = (zlo + zq) * P2 + y * P + x;
-      __half2 acc = z2, uc = z2;
-      if (DEF || !from_zero) {
-        int t = 0;
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+      const int y = 1 + k / hp, x = 2 * (k - (y - 1) * hp);
+      for (int zq = 0; zq < nz; ++zq) {
+        const uint32_t off = 2u * (uint32_t)((zlo + zq) * P2 + y * P + x);
+        __half2 acc = z2, uc = z2;
+        if (DEF || !from_zero) {
 #pragma unroll
-        for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll
-          for (int dy = -1; dy <= 1; ++dy, t += 3) {
-            const uint32_t* row = reinterpret_cast<const uint32_t*>(u + i + dz * P2 + dy * P);
-            const uint32_t w0 = row[-1], w1 = row[0], w2 = row[1];
+          for (int rw = 0; rw < 9; ++rw) {
+            const uint32_t a0 = su + off + (uint32_t)roff[rw];
+            uint32_t w0, w1, w2;
+            asm volatile("ld.shared.u32 %0, [%1+-4];" : "=r"(w0) : "r"(a0));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w1) : "r"(a0));
+            asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(w2) : "r"(a0));
             const __half2 lft = u2h(__byte_perm(w0, w1, 0x5432)), rgt = u2h(__byte_perm(w1, w2, 0x5432));
-            acc = fma16<FTZ, FMA>(t2[t], lft, acc);
-            acc = fma16<FTZ, FMA>(t2[t + 1], u2h(w1), acc);
-            acc = fma16<FTZ, FMA>(t2[t + 2], rgt, acc);
-            if (dz == 0 && dy == 0) uc = u2h(w1);
+            acc = fma16<FTZ, FMA>(t2[3 * rw], lft, acc);
+            acc = fma16<FTZ, FMA>(t2[3 * rw + 1], u2h(w1), acc);
+            acc = fma16<FTZ, FMA>(t2[3 * rw + 2], rgt, acc);
+            if (rw == 4) uc = u2h(w1);
           }
+        }
+        uint32_t bw;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(bw) : "r"(sb + off));
+        const __half2 r = fma16<FTZ, FMA>(m1, acc, u2h(bw));
+        __half2 out = DEF ? r : fma16<FTZ, FMA>(w, mul16<FTZ>(d, r), uc);
+        uint32_t ow = h2u(out);
+        if (x == 0) ow &= 0xFFFF0000u;  // ghost node stays +0
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(so + off), "r"(ow) : "memory");
       }
-      const __half2 bb = u2h(*reinterpret_cast<const uint32_t*>(b + i));
-      const __half2 r = fma16<FTZ, FMA>(m1, acc, bb);
-      __half2 out = DEF ? r : fma16<FTZ, FMA>(w, mul16<FTZ>(d, r), uc);
-      if (x == 0) out = u2h(h2u(out) & 0xFFFF0000u);  // ghost node stays +0
-      *reinterpret_cast<uint32_t*>(o + i) = h2u(out);
     }
   }
   __device__ bool pairs_ok(const CoarseLevel& L) const {
@@ -427,8 +467,7 @@ struct Coarse {
     // slab mode: coarse plane k is computed by the owner of fine plane 2k
     // (and written to CTA 0's shared memory when the coarse level is a CTA-0 level)
     const int mode = (slab && !small(F)) ? 2 : ((spread || !small(C)) ? 1 : 0);
-    for_points_by(C, mode, [&](int ci, int Pc) {
-      const int cx = ci % Pc, cy = (ci / Pc) % Pc, cz = F.dim == 3 ? ci / (Pc * Pc) : 0;
+    for_points_xyz(C, mode, [&](int ci, int cx, int cy, int cz, int Pc) {
       const int cf = cz * 2 * pf + cy * 2 * Pf + cx * 2;
       T acc = OF::zero();
       for (int dz = (F.dim == 3 ? -1 : 0); dz <= (F.dim == 3 ? 1 : 0); ++dz)
@@ -462,8 +501,7 @@ struct Coarse {
     const TC* cc = static_cast<const TC*>(ccv);
     TF* uf = static_cast<TF*>(ufv);
     const int Pc = C.nodes - 1;
-    for_points(F, [&](int fi, int Pf) {
-      const int fx = fi % Pf, fy = (fi / Pf) % Pf, fz = F.dim == 3 ? fi / (Pf * Pf) : 0;
+    for_points_xyz(F, small(F) ? 0 : (slab ? 2 : 1), [&](int fi, int fx, int fy, int fz, int Pf) {
       const int nx = (fx & 1) ? 2 : 1, ny = (fy & 1) ? 2 : 1, nz = F.dim == 3 ? ((fz & 1) ? 2 : 1) : 1;
       const int px[2] = {fx >> 1, (fx + 1) >> 1}, py[2] = {fy >> 1, (fy + 1) >> 1}, pz[2] = {fz >> 1, (fz + 1) >> 1};
       const TC w = OC::weight((fx & 1) + (fy & 1) + (F.dim == 3 ? (fz & 1) : 0));
