@@ -150,7 +150,8 @@ struct IrState {
   int refresh_now;    // next refresh due
   int pending;        // deferred corrections stored in the ring, not yet folded into u
   int fold_now;       // the current iteration folds the ring into u (refresh due or ring full)
-  int pad;
+  int final_pending;  // residual_norm still to compute (0: the last iteration's refresh defect
+                      // left exactly its partial sums in the buffer)
 };
 
 std::string& last_error();

@@ -67,7 +67,8 @@ struct Level {
 // applies ir_solver.cpp:95-120 to the device IR state
 __global__ void k_control(IrState* st, const double* p_main, int n_main, const double* p_ref, int n_ref,
                           double* hist, int hist_cap, double tol, int max_it, int scale_enabled, int refresh,
-                          int increment, cudaGraphConditionalHandle cond, int use_cond, int ring_k) {
+                          int increment, cudaGraphConditionalHandle cond, int use_cond, int ring_k,
+                          int reuse_refresh) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // pdl_wait (mpmg_arith.cuh)
   __shared__ double red[kCtlThreads];
   const bool ref = increment && st->refresh_now;
@@ -103,6 +104,10 @@ __global__ void k_control(IrState* st, const double* p_main, int n_main, const d
     // the next iteration folds the ring into u when it refreshes r = b - A u
     // or when its c fills the last slot
     st->fold_now = ring_k > 0 && (st->refresh_now || st->pending + 1 >= ring_k) ? 1 : 0;
+    // residual_norm (ir_solver.cpp:21-49) of an iterate whose refresh defect
+    // just ran is that defect's sum of squares: fma(-1, t, b) and b - t round
+    // identically and both use the FMA product A u
+    st->final_pending = (increment && ref && reuse_refresh) ? 0 : 1;
     if (use_cond) cudaGraphSetConditional(cond, active ? 1u : 0u);
   }
 }
@@ -117,6 +122,7 @@ __global__ void k_state_reset(IrState* st) {
   st->refresh_now = 0;
   st->pending = 0;
   st->fold_now = 0;
+  st->final_pending = 1;
 }
 
 __global__ void k_sanitize_scale(double* s) {
@@ -279,7 +285,7 @@ struct mpmg_solver {
     if (e == cudaSuccess) {
       k_control<<<1, kCtlThreads, 0, q>>>(st, partD, n0, partD, n0, hist, hist_cap, p.outer_tolerance,
                                             p.max_outer_iterations, scale_enabled(p),
-                                            p.residual_refresh_interval, 0, h, use_cond, ring_k);
+                                            p.residual_refresh_interval, 0, h, use_cond, ring_k, 0);
       e = cudaGetLastError();
     }
     return e;
@@ -307,7 +313,7 @@ struct mpmg_solver {
     if (e == cudaSuccess) {
       e = launch_pdl(k_control, dim3(1), dim3(kCtlThreads), 0, q, st, (const double*)partU, nU,
                      (const double*)partD, nD, hist, hist_cap, p.outer_tolerance, p.max_outer_iterations,
-                     scale_enabled(p), p.residual_refresh_interval, 1, h, use_cond, ring_k);
+                     scale_enabled(p), p.residual_refresh_interval, 1, h, use_cond, ring_k, fma() ? 1 : 0);
     }
     return e;
   }
@@ -316,7 +322,7 @@ struct mpmg_solver {
     cudaError_t e = cudaSuccess;
     if (ring_k > 0)  // corrections still parked
       e = launch_fold(len, u, ring, ring_len, lv.back().A.prec, ring_scale, &st->pending, 0, nullptr, fma(), q);
-    if (e == cudaSuccess) e = launch_defect64(A64, b, u, nullptr, partD, true, true, q);
+    if (e == cudaSuccess) e = launch_defect64(A64, b, u, nullptr, partD, true, true, q, &st->final_pending);
     if (e == cudaSuccess) e = launch_norm_finalize(partD, nD, final_d, q);
     return e;
   }

@@ -209,3 +209,20 @@ def test_deferred_corrections_bitwise(variant, refresh, max_it, tol, graph, monk
     assert same(u1.view(np.uint64), u0.view(np.uint64))
     assert same(r1.residual_history, r0.residual_history)
     assert r1.final_residual == r0.final_residual
+
+
+@pytest.mark.parametrize("refresh", [1, 3, 0])
+def test_final_residual_is_residual_norm(refresh):
+    """SolveReport.final_residual == residual_norm(A, u, b) (ir_solver.cpp:21-49) of
+    the returned u, whether the last iteration refreshed r (its defect's sum of
+    squares is reused) or not (a fresh residual-norm pass)."""
+    dim, n, L = 3, 33, 5
+    b = mg.problem_rhs(dim, n)
+    h = mg.Hierarchy(dim, n, L, "h_mg", ftz=False)
+    cfg = mg.IrConfig(outer_tolerance=1e-10 * float(np.linalg.norm(b)), residual_refresh_interval=refresh)
+    u, rep = h.ir_solve(b, cfg)
+    h.close()
+    cols, vals = O.stiffness(dim, n)
+    t = O.spmv(cols, vals, FP64, u, O.ctx(False))
+    r = b - t
+    assert rep.final_residual == pytest.approx(float(np.sqrt(np.dot(r, r))), rel=1e-12)
