@@ -110,7 +110,8 @@ cudaError_t launch_partials_sum(const double* partials, int n, double* out, cuda
 int norm2_partials(size_t len);
 cudaError_t launch_copy_sumsq(size_t len, const double* x, double* y, double* partials, cudaStream_t s);
 cudaError_t launch_fold(size_t len, double* u, const void* ring, long long ring_len, int prec, const double* scales,
-                        const int* count, int extra, const int* gate, bool fma, cudaStream_t s);
+                        const int* count, int extra, const int* gate, bool fma, cudaStream_t s,
+                        const int* uzero = nullptr);
 cudaError_t launch_fill_random01(double* padded_u, int dim, int nodes, uint64_t seed, cudaStream_t s);
 
 // ---- coarse sub-hierarchy (mpmg_coarse.cu) --------------------------------
@@ -152,6 +153,7 @@ struct IrState {
   int fold_now;       // the current iteration folds the ring into u (refresh due or ring full)
   int final_pending;  // residual_norm still to compute (0: the last iteration's refresh defect
                       // left exactly its partial sums in the buffer)
+  int u_zero;         // deferred corrections: u is still the zero initial guess (never written)
 };
 
 std::string& last_error();

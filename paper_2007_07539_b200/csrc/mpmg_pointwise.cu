@@ -746,21 +746,29 @@ __device__ __forceinline__ double widen(typename St<PREC>::T v) {
 // k = 0 .. *count + extra - 1 in slot order -- per element the exact sequence
 // of the u half of update_residuum_correction (kernels.cpp:300-341), so u is
 // bitwise what the per-iteration update would have produced
+// uzero (optional device flag): u is still the zero initial guess -- start
+// the chain from +0 instead of reading u (and write u even with no slot).
 template <int PREC, bool FMA>
 __global__ void k_fold8(double* __restrict__ u, const void* __restrict__ ring, long long ring_len,
                         const double* __restrict__ scales, const int* count, int extra, const int* gate,
-                        long long len) {
+                        long long len, const int* uzero) {
   pdl_wait();
   pdl_launch();
   if (gate && *gate == 0) return;
   const int n = *count + extra;
-  if (n <= 0) return;
+  const bool uz = uzero && *uzero;
+  if (n <= 0 && !uz) return;
   using T = typename St<PREC>::T;
   const T* cr = static_cast<const T*>(ring);
   const long long n8 = len / 8;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n8; g += (long long)gridDim.x * blockDim.x) {
     V8<P64> acc;
-    acc.load(u, 8 * g);
+    if (uz) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc.set(e, 0.0);
+    } else {
+      acc.load(u, 8 * g);
+    }
     for (int k = 0; k < n; ++k) {
       const double a = scales[k];
       V8<PREC> c;
@@ -772,14 +780,14 @@ __global__ void k_fold8(double* __restrict__ u, const void* __restrict__ ring, l
   }
   if (blockIdx.x == 0 && threadIdx.x < len - 8 * n8) {
     const long long i = 8 * n8 + threadIdx.x;
-    double v = u[i];
+    double v = uz ? 0.0 : u[i];
     for (int k = 0; k < n; ++k) v = fma64<FMA>(scales[k], widen<PREC>(cr[k * ring_len + i]), v);
     u[i] = v;
   }
 }
 
 cudaError_t launch_fold(size_t len, double* u, const void* ring, long long ring_len, int prec, const double* scales,
-                        const int* count, int extra, const int* gate, bool fma, cudaStream_t s) {
+                        const int* count, int extra, const int* gate, bool fma, cudaStream_t s, const int* uzero) {
   if (!aligned64(u) || !aligned64(ring) || (ring_len * mpmg_bytes_per_value(prec)) % 64 != 0)
     return cudaErrorInvalidValue;
   return with_prec(prec, [&](auto pc) -> cudaError_t {
@@ -788,9 +796,9 @@ cudaError_t launch_fold(size_t len, double* u, const void* ring, long long ring_
     const unsigned g = std::min<unsigned>(grid8(len), 148u * 4u);
     if (fma)
       return launch_pdl(k_fold8<PR, true>, dim3(g), dim3(kThreads), 0, s, u, ring, ring_len, scales, count, extra,
-                        gate, (long long)len);
+                        gate, (long long)len, uzero);
     return launch_pdl(k_fold8<PR, false>, dim3(g), dim3(kThreads), 0, s, u, ring, ring_len, scales, count, extra,
-                      gate, (long long)len);
+                      gate, (long long)len, uzero);
   });
 }
 

@@ -86,7 +86,10 @@ __global__ void k_control(IrState* st, const double* p_main, int n_main, const d
     const double alpha = sqrt(red[0]);
     // deferred corrections: this iteration stored one more c in the ring,
     // or folded all of them (and its own) into u
-    if (increment && ring_k > 0) st->pending = st->fold_now ? 0 : st->pending + 1;
+    if (increment && ring_k > 0) {
+      if (st->fold_now) st->u_zero = 0;
+      st->pending = st->fold_now ? 0 : st->pending + 1;
+    }
     if (increment) st->iterations += 1;
     const int it = st->iterations;
     if (hist && it < hist_cap) hist[it] = alpha;
@@ -112,7 +115,7 @@ __global__ void k_control(IrState* st, const double* p_main, int n_main, const d
   }
 }
 
-__global__ void k_state_reset(IrState* st) {
+__global__ void k_state_reset(IrState* st, int u_zero) {
   st->alpha = 0.0;
   st->scale = 1.0;
   st->iterations = 0;
@@ -123,6 +126,7 @@ __global__ void k_state_reset(IrState* st) {
   st->pending = 0;
   st->fold_now = 0;
   st->final_pending = 1;
+  st->u_zero = u_zero;
 }
 
 __global__ void k_sanitize_scale(double* s) {
@@ -271,9 +275,12 @@ struct mpmg_solver {
   }
 
   cudaError_t enqueue_init(const mpmg_solve_params& p, cudaStream_t q, cudaGraphConditionalHandle h, int use_cond) {
-    k_state_reset<<<1, 1, 0, q>>>(st);
+    // deferred corrections from u0 = 0: u is first written by a fold, which
+    // starts from +0 instead of reading it (no zero fill, no first read)
+    const int uz = ring_k > 0 && !p.random_initial_guess;
+    k_state_reset<<<1, 1, 0, q>>>(st, uz);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemsetAsync(u, 0, len * sizeof(double), q);
+    if (e == cudaSuccess && !uz) e = cudaMemsetAsync(u, 0, len * sizeof(double), q);
     if (e == cudaSuccess && p.random_initial_guess)
       e = launch_fill_random01(u, cfg.dim, cfg.nodes, p.seed, q);
     int n0 = nD;  // ir_solver.cpp:92-93: r = b - A u
@@ -304,7 +311,7 @@ struct mpmg_solver {
                                               ring_scale, fma(), q, &e))
         e = cudaErrorInvalidValue;
       if (e == cudaSuccess)
-        e = launch_fold(len, u, ring, ring_len, fp, ring_scale, &st->pending, 1, &st->fold_now, fma(), q);
+        e = launch_fold(len, u, ring, ring_len, fp, ring_scale, &st->pending, 1, &st->fold_now, fma(), q, &st->u_zero);
     } else if (e == cudaSuccess) {  // ir_solver.cpp:112
       e = launch_update_rc(A64, c, fp, r, u, &st->scale, partU, fma(), q);
     }
@@ -321,7 +328,8 @@ struct mpmg_solver {
   cudaError_t enqueue_final(cudaStream_t q) {  // residual_norm, ir_solver.cpp:21-49 / :122
     cudaError_t e = cudaSuccess;
     if (ring_k > 0)  // corrections still parked
-      e = launch_fold(len, u, ring, ring_len, lv.back().A.prec, ring_scale, &st->pending, 0, nullptr, fma(), q);
+      e = launch_fold(len, u, ring, ring_len, lv.back().A.prec, ring_scale, &st->pending, 0, nullptr, fma(), q,
+                      &st->u_zero);
     if (e == cudaSuccess) e = launch_defect64(A64, b, u, nullptr, partD, true, true, q, &st->final_pending);
     if (e == cudaSuccess) e = launch_norm_finalize(partD, nD, final_d, q);
     return e;
