@@ -71,6 +71,10 @@ bool plane_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void
                         uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
 bool plane_level_op_f64(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                         uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
+bool plane_jacobi_slot_f16(const mpmg_stencil& A, const void* x, const void* b, void* ring, long long stride,
+                           const int* slot, double omega, uint32_t policy, cudaStream_t s, cudaError_t* err);
+bool plane_jacobi_slot_f32(const mpmg_stencil& A, const void* x, const void* b, void* ring, long long stride,
+                           const int* slot, double omega, uint32_t policy, cudaStream_t s, cudaError_t* err);
 bool plane_defect64(const mpmg_stencil& A64, const double* b, const double* u, double* r, double* partials,
                     bool fma, bool resnorm, cudaStream_t s, const int* gate, cudaError_t* err,
                     const mpmg_slab* slab = nullptr);

@@ -68,6 +68,11 @@ struct PlaneArgs {
   long long ring_len;
   const int* ring_slot; // UPDATE_R: device slot index
   double* ring_scale;   // UPDATE_R: per-slot scale (= *alpha)
+  // optional: out += *out_slot * out_stride values (a Jacobi step writing
+  // straight into the correction ring); UPDATE_R with x == nullptr reads c
+  // from ring slot *ring_slot and skips the copy
+  const int* out_slot;
+  long long out_stride;
 };
 
 // ---- PTX: mbarrier + bulk copy ------------------------------------------
@@ -488,6 +493,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
   const int xrows = min(y0 + TY, P) - y0 + 2;  // operand rows y0-1 .. min(y0+TY, P)
   const int erows = min(TY, P - y0);           // epilogue rows y0 .. y0+erows-1
 
+  const unsigned char* xsrc = static_cast<const unsigned char*>(a.x);  // set after the gate (ring slot)
   auto issue = [&](int k) {  // one elected thread: plane k into stage k % NS
     const int q = z0 - 1 + k;
     if ((q == 0 && !a.load_lo) || (q == a.pz && !a.load_hi)) return;  // zero ghost planes are never loaded
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
     else if constexpr (K::kB && !K::kBReg) tot += eb;
     mbar_arrive_tx(bar, tot);
     const long long xo = q * plane + (long long)(y0 - 1) * P;
-    bulk_g2s(st, static_cast<const unsigned char*>(a.x) + xo * Bytes<LP>::v, xb, bar);
+    bulk_g2s(st, xsrc + xo * Bytes<LP>::v, xb, bar);
     const long long eo = q * plane + (long long)y0 * P;
     if constexpr (OP == POP_UPDATE) {
       bulk_g2s(st + K::kXBytes, a.r64 + eo, (uint32_t)(erows * P * 8), bar);
@@ -523,11 +529,17 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
   }
   __syncthreads();
   long long ring_off = 0;
+  bool ring_copy = false;
   if constexpr (OP == POP_UPDATE_R) {
     const int slot = *a.ring_slot;
     ring_off = (long long)slot * a.ring_len;
     if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) a.ring_scale[slot] = *a.alpha;
+    ring_copy = a.x != nullptr;
+    if (!ring_copy) xsrc = static_cast<const unsigned char*>(a.ring) + ring_off * Bytes<LP>::v;
   }
+  void* const outp = a.out_slot ? static_cast<void*>(static_cast<unsigned char*>(a.out) +
+                                                      (long long)*a.out_slot * a.out_stride * Bytes<EP>::v)
+                                : a.out;
   if (tid == 0) {
     for (int k = 0; k < NS - 1 && k < NQ; ++k) issue(k);
   }
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
       else if constexpr (EP == P16) t = quant16<FTZ, W>(Acc[i]);
       if constexpr (OP == POP_SPMV) {
         if (x0 == 0) rzero_first<EP, W>(t);
-        if (v) gstore<EP, W>(a.out, gi, t);
+        if (v) gstore<EP, W>(outp, gi, t);
       } else if constexpr (OP == POP_DEFECT || OP == POP_JACOBI || OP == POP_JACOBI_Z) {
         Row<EP, W> bb;
         if constexpr (K::kJZ) rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, bb);  // b centre
@@ -649,7 +661,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
           Row<EP, W> r = efma<EP, FTZ, FMA, W>(m1, t, bb);  // axpy(-1, t, b)
           if constexpr (OP == POP_DEFECT) {
             if (x0 == 0) rzero_first<EP, W>(r);
-            if (v) gstore<EP, W>(a.out, gi, r);
+            if (v) gstore<EP, W>(outp, gi, r);
           } else {
             const Row<EP, W> dr = emul<EP, FTZ, W>(a.d16, r);  // vec_multiply(inv_diag, r)
             Row<EP, W> uc;
@@ -659,7 +671,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
             } else rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
             Row<EP, W> un = efma<EP, FTZ, FMA, W>(a.w16, dr, uc);  // axpy(omega, t, u)
             if (x0 == 0) rzero_first<EP, W>(un);
-            if (v) gstore<EP, W>(a.out, gi, un);
+            if (v) gstore<EP, W>(outp, gi, un);
           }
         } else {
           using ET = typename Sc<EP>::T;
@@ -667,7 +679,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
           Row<EP, W> r = efma<EP, FTZ, FMA, W>(m1, t, bb);
           if constexpr (OP == POP_DEFECT) {
             if (x0 == 0) rzero_first<EP, W>(r);
-            if (v) gstore<EP, W>(a.out, gi, r);
+            if (v) gstore<EP, W>(outp, gi, r);
           } else {
             const Row<EP, W> dr = emul<EP, FTZ, W>(dd, r);
             Row<EP, W> uc;
@@ -677,7 +689,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
             } else rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
             Row<EP, W> un = efma<EP, FTZ, FMA, W>(ww, dr, uc);
             if (x0 == 0) rzero_first<EP, W>(un);
-            if (v) gstore<EP, W>(a.out, gi, un);
+            if (v) gstore<EP, W>(outp, gi, un);
           }
         }
       } else if constexpr (OP == POP_DEFECT64 || OP == POP_RESNORM) {
@@ -688,7 +700,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
           r.v[e] = OP == POP_RESNORM ? __dsub_rn(bb.v[e], t.v[e]) : fma64<FMA>(-1.0, t.v[e], bb.v[e]);
         if (x0 == 0) rzero_first<P64, W>(r);
         if (v) {
-          if (OP == POP_DEFECT64 && a.out) gstore<P64, W>(a.out, gi, r);
+          if (OP == POP_DEFECT64 && a.out) gstore<P64, W>(outp, gi, r);
 #pragma unroll
           for (int e = 0; e < W; ++e) sq = __fma_rn(r.v[e], r.v[e], sq);
         }
@@ -703,7 +715,7 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
         if (x0 == 0) rzero_first<P64, W>(rn);
         if (v) {
           gstore<P64, W>(a.r64, gi, rn);
-          gstore<LP, W>(a.ring, ring_off + gi, craw);  // c unchanged (x = 0 ghost is zero)
+          if (ring_copy) gstore<LP, W>(a.ring, ring_off + gi, craw);  // c unchanged (x = 0 ghost is zero)
 #pragma unroll
           for (int e = 0; e < W; ++e) sq = __fma_rn(rn.v[e], rn.v[e], sq);
         }
@@ -818,6 +830,9 @@ __global__ void __launch_bounds__(128) k_direct(const __grid_constant__ PlaneArg
   }();
   (void)jd; (void)jw;
   const long long gi = z * plane + (long long)y * P + x0;
+  void* const outp = a.out_slot ? static_cast<void*>(static_cast<unsigned char*>(a.out) +
+                                                      (long long)*a.out_slot * a.out_stride * Bytes<LP>::v)
+                                : a.out;
   Row<LP, W> acc, ctr;
   rzero(acc);
   rzero(ctr);
@@ -849,24 +864,24 @@ __global__ void __launch_bounds__(128) k_direct(const __grid_constant__ PlaneArg
     Row<LP, W> r = efma<LP, FTZ, FMA, W>(m1, acc, bb);
     if constexpr (OP == POP_DEFECT) {
       if (x0 == 0) rzero_first<LP, W>(r);
-      gstore<LP, W>(a.out, gi, r);
+      gstore<LP, W>(outp, gi, r);
     } else {
       const Row<LP, W> dr = emul<LP, FTZ, W>(a.d16, r);
       Row<LP, W> un = efma<LP, FTZ, FMA, W>(a.w16, dr, ctr);  // ctr: u, or u1 = w D^-1 b (JACOBI_Z)
       if (x0 == 0) rzero_first<LP, W>(un);
-      gstore<LP, W>(a.out, gi, un);
+      gstore<LP, W>(outp, gi, un);
     }
   } else {
     const ST m1 = ST(-1), dd = LP == P32 ? (ST)a.d32 : (ST)a.d64, ww = LP == P32 ? (ST)a.w32 : (ST)a.w64;
     Row<LP, W> r = efma<LP, FTZ, FMA, W>(m1, acc, bb);
     if constexpr (OP == POP_DEFECT) {
       if (x0 == 0) rzero_first<LP, W>(r);
-      gstore<LP, W>(a.out, gi, r);
+      gstore<LP, W>(outp, gi, r);
     } else {
       const Row<LP, W> dr = emul<LP, FTZ, W>(dd, r);
       Row<LP, W> un = efma<LP, FTZ, FMA, W>(ww, dr, ctr);
       if (x0 == 0) rzero_first<LP, W>(un);
-      gstore<LP, W>(a.out, gi, un);
+      gstore<LP, W>(outp, gi, un);
     }
   }
 }

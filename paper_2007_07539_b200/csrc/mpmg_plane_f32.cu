@@ -6,4 +6,9 @@ bool plane_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void
                        uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab) {
   return plane_level_op<mpmg_dev::P32>(op, A, x, b, out, omega, policy, s, err, slab);
 }
+// one Jacobi step whose output goes to slot *slot of a ring (stride values)
+bool plane_jacobi_slot_f32(const mpmg_stencil& A, const void* x, const void* b, void* ring, long long stride,
+                          const int* slot, double omega, uint32_t policy, cudaStream_t s, cudaError_t* err) {
+  return plane_level_op<mpmg_dev::P32>(2, A, x, b, ring, omega, policy, s, err, nullptr, slot, stride);
+}
 }  // namespace mpmg_impl

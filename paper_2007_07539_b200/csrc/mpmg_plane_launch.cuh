@@ -189,7 +189,8 @@ inline bool faces_zero16(const mpmg_stencil& A) {
 // the plane kernels; false if not covered
 template <int LP>
 bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
-                    uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr) {
+                    uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr,
+                    const int* out_slot = nullptr, long long out_stride = 0) {
   if (A.dim != 3 || (op != 1 && op != 2 && op != 3)) return false;
   if (pitch(A.nodes) < plane_min_pitch()) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
@@ -197,6 +198,7 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
   if (!aligned16(x) || !aligned16(b) || !aligned16(out)) return false;
   PlaneArgs a = plane_args(A, slab);
   a.x = x; a.b = b; a.out = out;
+  a.out_slot = out_slot; a.out_stride = out_stride;
   const bool ftz = policy & MPMG_FTZ;
   const double w = round_to(omega, LP, ftz);
   a.w16 = h2_of(w); a.w32 = (float)w; a.w64 = w;

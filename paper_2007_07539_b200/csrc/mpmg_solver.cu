@@ -161,6 +161,7 @@ struct mpmg_solver {
   // per element the same fma sequence, so u is bitwise unchanged, while each
   // iteration skips the FP64 read + write of u (16 of 34 bytes per unknown)
   int ring_k = 0;  // 0: fused update (FP64 finest level or unsupported shape)
+  bool ring_cycle = false;  // while enqueueing an IR iteration: the V-cycle may end in the ring
   void* ring = nullptr;
   long long ring_len = 0;
   double* ring_scale = nullptr;
@@ -258,6 +259,19 @@ struct mpmg_solver {
     e = launch_prolong(L.A.dim, L.A.nodes, L.A.prec, C.A.prec, cc, cur, sc, policy(), q);
     for (int k = 0; k < cfg.post_steps && e == cudaSuccess; ++k) {
       void* out = (cur == L.u) ? L.u2 : L.u;
+      if (ring_cycle && l == finest() && k == cfg.post_steps - 1) {
+        // the correction goes straight into the deferred-correction ring slot
+        // (read there by UPDATE_R, which then skips its copy)
+        bool done = false;
+        if (L.A.prec == MPMG_FP16)
+          done = plane_jacobi_slot_f16(L.A, cur, L.b, ring, ring_len, &st->pending, cfg.omega, policy(), q, &e);
+        else if (L.A.prec == MPMG_FP32)
+          done = plane_jacobi_slot_f32(L.A, cur, L.b, ring, ring_len, &st->pending, cfg.omega, policy(), q, &e);
+        if (done) {
+          *result = nullptr;
+          return e;
+        }
+      }
       e = launch_level_op(2, L.A, cur, L.b, out, cfg.omega, policy(), q);
       cur = out;
     }
@@ -305,7 +319,9 @@ struct mpmg_solver {
     if (!rlow_alias)  // cast_vector(r, mg_precision, scale, r_low), ir_solver.cpp:109-110
       e = launch_downcast(cfg.dim, cfg.nodes, r, rlow, fp, &st->scale, 1, policy(), q);
     void* c = nullptr;
-    if (e == cudaSuccess) e = v_cycle(q, &c);  // ir_solver.cpp:111
+    ring_cycle = ring_k > 0;
+    if (e == cudaSuccess) e = v_cycle(q, &c);  // ir_solver.cpp:111 (c == nullptr: in the ring slot)
+    ring_cycle = false;
     if (ring_k > 0) {  // ir_solver.cpp:112, the u half deferred
       if (e == cudaSuccess && !plane_update_r(A64, c, fp, r, &st->scale, partU, ring, ring_len, &st->pending,
                                               ring_scale, fma(), q, &e))
