@@ -447,7 +447,8 @@ __device__ __forceinline__ bool is_face(int k) {
 // LP storage precision of the stencil operand; CP accumulation precision;
 // EP epilogue/output precision; W values per lane; WX warps per row;
 // WY warp-rows per CTA; RY rows per thread; NS pipeline stages.
-// OPT bit 0: stage b through shared memory (instead of the register prefetch)
+// OPT bit 0: stage b through shared memory (instead of the register prefetch);
+// bit 2: output to ring slot *out_slot (PlaneArgs::out_slot / out_stride)
 template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, bool SKIPF, int W, int WX, int WY, int RY, int NS,
           int OPT = 0>
 struct PlaneK {
@@ -537,9 +538,11 @@ __global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ 
     ring_copy = a.x != nullptr;
     if (!ring_copy) xsrc = static_cast<const unsigned char*>(a.ring) + ring_off * Bytes<LP>::v;
   }
-  void* const outp = a.out_slot ? static_cast<void*>(static_cast<unsigned char*>(a.out) +
-                                                      (long long)*a.out_slot * a.out_stride * Bytes<EP>::v)
-                                : a.out;
+  // OPT bit 2: the output goes to slot *out_slot of a ring (a separate
+  // instantiation, so the common kernels carry no extra registers)
+  void* outp = a.out;
+  if constexpr ((OPT & 4) != 0)
+    outp = static_cast<unsigned char*>(a.out) + (long long)*a.out_slot * a.out_stride * Bytes<EP>::v;
   if (tid == 0) {
     for (int k = 0; k < NS - 1 && k < NQ; ++k) issue(k);
   }
@@ -830,9 +833,7 @@ __global__ void __launch_bounds__(128) k_direct(const __grid_constant__ PlaneArg
   }();
   (void)jd; (void)jw;
   const long long gi = z * plane + (long long)y * P + x0;
-  void* const outp = a.out_slot ? static_cast<void*>(static_cast<unsigned char*>(a.out) +
-                                                      (long long)*a.out_slot * a.out_stride * Bytes<LP>::v)
-                                : a.out;
+  void* const outp = a.out;
   Row<LP, W> acc, ctr;
   rzero(acc);
   rzero(ctr);

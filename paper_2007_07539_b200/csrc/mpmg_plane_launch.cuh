@@ -28,7 +28,7 @@ struct PlaneCfg {
   static constexpr int RY = V == 1 ? 2 : (V == 2 ? 2 : (V == 3 ? 4 : (V == 5 ? 1 : RY0)));
   static constexpr int WY = V == 2 ? 8 : (V == 3 ? 2 : (V == 5 ? 8 : WY0));
   static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : (V == 10 ? 4 : NS0));
-  static constexpr int OPT = V == 4 ? 1 : 0;
+  static constexpr int OPT = V == 4 ? 1 : (V == 11 ? 4 : 0);
 };
 
 inline int plane_variant() {
@@ -204,6 +204,11 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
   a.w16 = h2_of(w); a.w32 = (float)w; a.w64 = w;
   return with_pitch(a.P, [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
+    if (out_slot) {  // Jacobi step into a ring slot (V = 11: the OPT bit-2 instantiation)
+      *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP, 11>::run(a, s)
+                 : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 11>::run(a, s);
+      return;
+    }
     if constexpr (PP <= 256) {
       if (!slab && PP <= direct_max_pitch()) {  // small L2-resident level: direct loads
         constexpr int W = PP / 32;
