@@ -472,7 +472,8 @@ struct PlaneK {
 
 template <int LP, int CP, int EP, int OP, bool FTZ, bool FMA, bool SKIPF, int W, int WX, int WY, int RY, int NS,
           int OPT = 0>
-__global__ void __launch_bounds__(32 * WX * WY) k_plane(const __grid_constant__ PlaneArgs a) {
+__global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 128) ? 4 : 1)
+    k_plane(const __grid_constant__ PlaneArgs a) {
   using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, W, WX, WY, RY, NS, OPT>;
   using ST = typename Sc<CP>::T;
   constexpr int P = K::kP;
