@@ -155,6 +155,13 @@ int mpmg_gpu_update_r(const mpmg_stencil* A64, const void* c, int32_t c_prec, do
                       double* partials, void* ring, int64_t ring_len, const int32_t* slot_dev, double* ring_scale,
                       uint32_t policy, void* stream);
 int mpmg_gpu_update_r_partials(int32_t dim, int32_t nodes, int32_t c_prec);
+/* The last finest post-smoothing step of a deferred-correction cycle
+ * (jacobi_smooth, multigrid.cpp:79-89, one step): u_out = the Jacobi step of
+ * u_in written straight into ring slot *slot_dev (ring + *slot_dev *
+ * ring_len values), where update_r then reads c. binary16/32 3D levels with
+ * pitch 32..1024 and FMA on; MPMG_EUNSUPPORTED otherwise. */
+int mpmg_gpu_jacobi_slot(const mpmg_stencil* A, const void* b, const void* u_in, void* ring, int64_t ring_len,
+                         const int32_t* slot_dev, double omega, uint32_t policy, void* stream);
 int mpmg_gpu_fold(int64_t len, double* u, const void* ring, int64_t ring_len, int32_t c_prec,
                   const double* ring_scale, const int32_t* count_dev, uint32_t policy, void* stream);
 

@@ -56,11 +56,17 @@ class _Ctx(C.Structure):
 
 class _Ell(C.Structure):
     _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("rw", C.c_int), ("prec", C.c_int),
-                ("col", C.POINTER(C.c_int32)), ("val", C.POINTER(C.c_double))]
+                ("col", C.POINTER(C.c_int32)), ("val", C.POINTER(C.c_double)),
+                ("gen", C.c_int), ("gdim", C.c_int), ("gn", C.c_int), ("gtaps", C.c_double * 27)]
 
 
-def _ell_to_numpy(e: _Ell):
+def _ell_to_numpy(e: _Ell, lib=None):
     n = e.rows * e.rw
+    if e.gen:  # implicit operator: generate the rows
+        cols = np.zeros((e.rows, e.rw), dtype=np.int32)
+        vals = np.zeros((e.rows, e.rw))
+        lib.orc_ell_rows(C.byref(e), cols, vals)
+        return cols, vals
     cols = np.ctypeslib.as_array(e.col, shape=(n,)).copy().reshape(e.rows, e.rw)
     vals = np.ctypeslib.as_array(e.val, shape=(n,)).copy().reshape(e.rows, e.rw)
     return cols, vals
@@ -95,6 +101,10 @@ class Oracle:
         L.orc_rhs.argtypes = [i, i, i, _dp]
         L.orc_exact.argtypes = [i, i, i, _dp]
         L.orc_ell_free.argtypes = [C.POINTER(_Ell)]
+        L.orc_ell_rows.argtypes = [C.POINTER(_Ell), _ip, _dp]
+        L.orc_stiffness_implicit.restype = i; L.orc_stiffness_implicit.argtypes = [i, i, C.POINTER(_Ell)]
+        L.orc_hier_build_ex.restype = C.c_void_p
+        L.orc_hier_build_ex.argtypes = [i, i, i, i, i, i, d, d, i, i, i, i, C.POINTER(C.c_int), i]
         L.orc_hier_build.restype = C.c_void_p
         L.orc_hier_build.argtypes = [i, i, i, i, i, i, d, d, i, i, i, i, C.POINTER(C.c_int)]
         L.orc_hier_free.argtypes = [C.c_void_p]
@@ -142,6 +152,14 @@ class Oracle:
         k = self.L.orc_stencil(dim, n, taps)
         return taps[:k].copy()
 
+    def stiffness_implicit(self, dim, n):
+        """The FP64 operator as an implicit row generator (bitwise the
+        assembled ELL; for 257^3 and up, where the slot arrays are GBs)."""
+        e = _Ell()
+        if self.L.orc_stiffness_implicit(dim, n, C.byref(e)):
+            raise ValueError("stiffness")
+        return e
+
     def transfer(self, dim, nf):
         P, R = _Ell(), _Ell()
         if self.L.orc_transfer(dim, nf, C.byref(P), C.byref(R)):
@@ -174,6 +192,22 @@ class Oracle:
         self.L.orc_spmv(C.byref(e), np.ascontiguousarray(x, dtype=np.float64), y, ctx or self.ctx())
         return y
 
+    # --- kernels on an _Ell (explicit or implicit, e.g. stiffness_implicit)
+    def spmv_e(self, e, x, ctx=None):
+        y = np.zeros(e.rows)
+        self.L.orc_spmv(C.byref(e), np.ascontiguousarray(x, dtype=np.float64), y, ctx or self.ctx())
+        return y
+
+    def update_rc_e(self, e, r, u, c, alpha, ctx=None):
+        r = np.array(r, dtype=np.float64); u = np.array(u, dtype=np.float64)
+        self.L.orc_update_rc(r, u, C.byref(e), np.ascontiguousarray(c, dtype=np.float64), float(alpha),
+                             ctx or self.ctx())
+        return r, u
+
+    def residual_norm_e(self, e, u, b):
+        return self.L.orc_residual_norm(C.byref(e), np.ascontiguousarray(u, dtype=np.float64),
+                                        np.ascontiguousarray(b, dtype=np.float64))
+
     def update_rc(self, cols, vals, r, u, c, alpha, ctx=None):
         cols = np.ascontiguousarray(cols, dtype=np.int32); vals = np.ascontiguousarray(vals, dtype=np.float64)
         rows, rw = cols.shape
@@ -204,21 +238,22 @@ class Oracle:
         return out
 
     def hierarchy(self, dim, n, levels, variant, pre=3, post=3, omega=2.0 / 3.0, base_tol=1e-4, base_mode=0,
-                  base_maxit=0, ftz=True, fma=True):
+                  base_maxit=0, ftz=True, fma=True, implicit=False):
         return OracleHierarchy(self, dim, n, levels, variant, pre, post, omega, base_tol, base_mode, base_maxit,
-                               ftz, fma)
+                               ftz, fma, implicit)
 
 
 class OracleHierarchy:
     def __init__(self, o: Oracle, dim, n, levels, variant, pre, post, omega, base_tol, base_mode, base_maxit,
-                 ftz, fma):
+                 ftz, fma, implicit=False):
         self.o, self.dim, self.n, self.L = o, dim, n, levels
+        self.implicit = bool(implicit)
         err = C.c_int(-1)
         if isinstance(variant, str):
             variant = VARIANTS[variant]
         self.variant = variant
-        self.h = o.L.orc_hier_build(dim, n, levels, variant, pre, post, omega, base_tol, base_mode, base_maxit,
-                                    int(ftz), int(fma), C.byref(err))
+        self.h = o.L.orc_hier_build_ex(dim, n, levels, variant, pre, post, omega, base_tol, base_mode,
+                                       base_maxit, int(ftz), int(fma), C.byref(err), int(implicit))
         if not self.h:
             raise RuntimeError(f"oracle hierarchy build failed (level {err.value})")
 
@@ -237,7 +272,7 @@ class OracleHierarchy:
         p = self.o.L.orc_level_matrix(self.h, l, which)
         if not p:
             return None
-        return _ell_to_numpy(p.contents)
+        return _ell_to_numpy(p.contents, self.o.L)
 
     def invdiag(self, l):
         p = self.o.L.orc_level_invdiag(self.h, l)
@@ -276,12 +311,16 @@ class OracleHierarchy:
     def ir_solve(self, b, A=None, tol=None, rel_tol=1e-10, max_it=100, random_guess=False, seed=0, scaling=0,
                  refresh=10, ctx=None):
         """Returns dict(iterations, history, converged, final_residual, u)."""
-        if A is None:
-            A = self.o.stiffness(self.dim, self.n)
-        cols = np.ascontiguousarray(A[0], dtype=np.int32); vals = np.ascontiguousarray(A[1], dtype=np.float64)
-        rows, rw = cols.shape
-        e = _Ell(rows, rows, rw, FP64, cols.ctypes.data_as(C.POINTER(C.c_int32)),
-                 vals.ctypes.data_as(C.POINTER(C.c_double)))
+        if A is None and self.implicit:
+            e = self.o.stiffness_implicit(self.dim, self.n)
+            rows = e.rows
+        else:
+            if A is None:
+                A = self.o.stiffness(self.dim, self.n)
+            cols = np.ascontiguousarray(A[0], dtype=np.int32); vals = np.ascontiguousarray(A[1], dtype=np.float64)
+            rows, rw = cols.shape
+            e = _Ell(rows, rows, rw, FP64, cols.ctypes.data_as(C.POINTER(C.c_int32)),
+                     vals.ctypes.data_as(C.POINTER(C.c_double)))
         b = np.ascontiguousarray(b, dtype=np.float64)
         if tol is None:
             tol = rel_tol * self.o.norm2(b)

@@ -111,6 +111,7 @@ static double ar_mul(int prec, double a, double b, orc_ctx x) {
 
 /* ell_matrix.cpp:10-28: every slot padded (value 0, col = min(row, cols-1)) */
 int orc_ell_alloc(orc_ell* m, int64_t rows, int64_t cols, int rw, int prec) {
+  memset(m, 0, sizeof(*m));
   m->rows = rows; m->cols = cols; m->rw = rw; m->prec = prec;
   m->col = (int32_t*)malloc((size_t)(rows * rw) * sizeof(int32_t));
   m->val = (double*)calloc((size_t)(rows * rw), sizeof(double));
@@ -148,6 +149,106 @@ static int ell_cast(const orc_ell* src, orc_ell* dst, int prec, int ftz) {
   return 0;
 }
 
+/* Implicit operators: row r generated in the slot order and padding of the
+ * assembled matrices. A: orc_stiffness below (mesh_fem.cpp:124-150): the
+ * in-domain neighbours in lexicographic (dz, dy, dx) order carrying the
+ * level's per-offset coefficient, then (col = row, 0) padding. P / R:
+ * orc_transfer (mesh_fem.cpp:204-295). */
+static void decode_row(int dim, int n, int64_t r, int* ix, int* iy, int* iz) {
+  const int64_t m = n - 2;
+  *ix = (int)(r % m) + 1;
+  *iy = (int)((r / m) % m) + 1;
+  *iz = dim == 3 ? (int)(r / (m * m)) + 1 : 1;
+}
+
+void orc_ell_row(const orc_ell* m, int64_t r, int32_t* cols, double* vals) {
+  const int rw = m->rw;
+  if (m->gen == 0) {
+    memcpy(cols, m->col + r * rw, (size_t)rw * sizeof(int32_t));
+    memcpy(vals, m->val + r * rw, (size_t)rw * sizeof(double));
+    return;
+  }
+  const int dim = m->gdim, n = m->gn;
+  int out = 0;
+  if (m->gen == 1) {
+    int ix, iy, iz;
+    decode_row(dim, n, r, &ix, &iy, &iz);
+    const int zlo = dim == 3 ? -1 : 0, zhi = dim == 3 ? 1 : 0;
+    for (int dz = zlo; dz <= zhi; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int jx = ix + dx, jy = iy + dy, jz = iz + dz;
+          if (!(jx >= 1 && jx <= n - 2) || !(jy >= 1 && jy <= n - 2) || (dim == 3 && !(jz >= 1 && jz <= n - 2)))
+            continue;
+          const int slot = ((dim == 3 ? dz + 1 : 0) * 3 + (dy + 1)) * 3 + (dx + 1);
+          const int64_t mm = n - 2;
+          cols[out] = (int32_t)((int64_t)(jy - 1) * mm + (jx - 1) + (dim == 3 ? (int64_t)(jz - 1) * mm * mm : 0));
+          vals[out++] = m->gtaps[slot];
+        }
+  } else if (m->gen == 2) { /* P: fine row, parents per dimension ascending */
+    const int nf = n, mc = (nf + 1) / 2 - 2;
+    int f[3];
+    decode_row(dim, nf, r, &f[0], &f[1], &f[2]);
+    int cnt[3], idx[3][2];
+    double w[3][2];
+    for (int d = 0; d < 3; ++d) {
+      if (d == 2 && dim == 2) { cnt[d] = 1; idx[d][0] = 1; w[d][0] = 1.0; continue; }
+      if (f[d] % 2 == 0) { cnt[d] = 1; idx[d][0] = f[d] / 2; w[d][0] = 1.0; }
+      else {
+        cnt[d] = 0;
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int jc = (f[d] - 1) / 2 + s2;
+          if (jc >= 1 && jc <= mc) { idx[d][cnt[d]] = jc; w[d][cnt[d]] = 0.5; ++cnt[d]; }
+        }
+      }
+    }
+    const int64_t mmc = mc;
+    for (int c = 0; c < cnt[2]; ++c)
+      for (int b = 0; b < cnt[1]; ++b)
+        for (int a = 0; a < cnt[0]; ++a) {
+          cols[out] = (int32_t)((int64_t)(idx[1][b] - 1) * mmc + (idx[0][a] - 1) +
+                                (dim == 3 ? (int64_t)(idx[2][c] - 1) * mmc * mmc : 0));
+          vals[out++] = orc_round(w[0][a] * w[1][b] * (dim == 3 ? w[2][c] : 1.0), m->prec, 0);
+        }
+  } else { /* R: coarse row, the 3^dim fine neighbours of node 2i */
+    const int nf = n, nc = (nf + 1) / 2;
+    int cx, cy, cz;
+    decode_row(dim, nc, r, &cx, &cy, &cz);
+    const int zlo = dim == 3 ? -1 : 0, zhi = dim == 3 ? 1 : 0;
+    const int64_t mf = nf - 2;
+    for (int dz = zlo; dz <= zhi; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          double ww = (dx == 0 ? 1.0 : 0.5) * (dy == 0 ? 1.0 : 0.5);
+          if (dim == 3) ww *= dz == 0 ? 1.0 : 0.5;
+          const int fx = 2 * cx + dx, fy = 2 * cy + dy, fz = dim == 3 ? 2 * cz + dz : 1;
+          cols[out] = (int32_t)((int64_t)(fy - 1) * mf + (fx - 1) + (dim == 3 ? (int64_t)(fz - 1) * mf * mf : 0));
+          vals[out++] = orc_round(ww, m->prec, 0);
+        }
+  }
+  const int32_t pc = (int32_t)(r < m->cols - 1 ? r : m->cols - 1); /* ell_matrix.cpp:90-92 */
+  for (; out < rw; ++out) { cols[out] = pc; vals[out] = 0.0; }
+}
+
+void orc_ell_rows(const orc_ell* m, int32_t* cols, double* vals) {
+  for (int64_t r = 0; r < m->rows; ++r) orc_ell_row(m, r, cols + r * m->rw, vals + r * m->rw);
+}
+
+/* row pointers without a copy for assembled matrices */
+#define ELL_ROW(m, r, c, v)                                           \
+  int32_t c##_buf[27];                                                \
+  double v##_buf[27];                                                 \
+  const int32_t* c;                                                   \
+  const double* v;                                                    \
+  if ((m)->gen == 0) {                                                \
+    c = (m)->col + (r) * (m)->rw;                                     \
+    v = (m)->val + (r) * (m)->rw;                                     \
+  } else {                                                            \
+    orc_ell_row((m), (r), c##_buf, v##_buf);                          \
+    c = c##_buf;                                                      \
+    v = v##_buf;                                                      \
+  }
+
 /* ------------------------------------------------------------------------ */
 /* sparse kernels (core/src/kernels.cpp)                                     */
 /* ------------------------------------------------------------------------ */
@@ -155,9 +256,9 @@ static int ell_cast(const orc_ell* src, orc_ell* dst, int prec, int ftz) {
 /* kernels.cpp:137-193 */
 void orc_spmv(const orc_ell* A, const double* x, double* y, orc_ctx ctx) {
   const int rw = A->rw;
+#pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < A->rows; ++r) {
-    const double* v = A->val + r * rw;
-    const int32_t* c = A->col + r * rw;
+    ELL_ROW(A, r, c, v)
     if (A->prec == ORC_FP16 && ctx.acc32) { /* kernels.cpp:151-162 */
       float acc = 0.0f;
       orc_ctx c32 = ctx;
@@ -174,21 +275,25 @@ void orc_spmv(const orc_ell* A, const double* x, double* y, orc_ctx ctx) {
 /* kernels.cpp:195-212: alpha rounded into the precision first */
 void orc_axpy(int prec, double alpha, const double* x, const double* y, double* out, int64_t n, orc_ctx ctx) {
   const double a = orc_round(alpha, prec, ctx.ftz);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = ar_fma(prec, a, x[i], y[i], ctx);
 }
 
 /* kernels.cpp:214-229 */
 void orc_vec_multiply(int prec, const double* a, const double* b, double* out, int64_t n, orc_ctx ctx) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = ar_mul(prec, a[i], b[i], ctx);
 }
 
 /* kernels.cpp:300-341: r, u, A binary64; c widened once */
 void orc_update_rc(double* r, double* u, const orc_ell* A, const double* c, double alpha, orc_ctx ctx) {
   const int rw = A->rw;
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < A->rows; ++i) {
     u[i] = ar_fma(ORC_FP64, alpha, c[i], u[i], ctx);
+    ELL_ROW(A, i, ac, av)
     double s = 0.0;
-    for (int j = 0; j < rw; ++j) s = ar_fma(ORC_FP64, A->val[i * rw + j], c[A->col[i * rw + j]], s, ctx);
+    for (int j = 0; j < rw; ++j) s = ar_fma(ORC_FP64, av[j], c[ac[j]], s, ctx);
     r[i] = ar_fma(ORC_FP64, -alpha, s, r[i], ctx);
   }
 }
@@ -196,6 +301,7 @@ void orc_update_rc(double* r, double* u, const orc_ell* A, const double* c, doub
 /* kernels.cpp:231-239, 343-360: division in binary64, one rounding */
 int orc_cast(const double* x, int64_t n, int target, double scale, double* out, orc_ctx ctx) {
   if (!(scale > 0.0) || !isfinite(scale)) return -1;
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = orc_round(x[i] / scale, target, ctx.ftz);
   return 0;
 }
@@ -476,8 +582,40 @@ static int variant_prec(int v, int l) {
 }
 
 /* multigrid.cpp:282-342 (ProblemSpec::validate: mesh_fem.cpp:57-69) */
+/* an implicit A / P / R of precision prec (the ell_cast rounding of the
+ * assembled FP64 values: the stencil taps; transfer weights are powers of 2) */
+static void implicit_ell(orc_ell* m, int gen, int dim, int n, int prec, int ftz) {
+  memset(m, 0, sizeof(*m));
+  const int nc = (n + 1) / 2;
+  const int64_t N = orc_unknowns(dim, n), Nc = gen == 1 ? N : orc_unknowns(dim, nc);
+  m->gen = gen; m->gdim = dim; m->gn = n; m->prec = prec;
+  if (gen == 1) {
+    m->rows = N; m->cols = N; m->rw = dim == 2 ? 9 : 27;
+    double t[27];
+    orc_stencil(dim, n, t);
+    for (int k = 0; k < m->rw; ++k) m->gtaps[k] = orc_round(t[k], prec, ftz);
+  } else {
+    m->rows = gen == 2 ? N : Nc; m->cols = gen == 2 ? Nc : N;
+    m->rw = gen == 2 ? (1 << dim) : (dim == 2 ? 9 : 27);
+    (void)ftz; /* transfer weights are powers of two >= 2^-3: exact in every precision */
+  }
+}
+
+int orc_stiffness_implicit(int dim, int n, orc_ell* A) {
+  if ((dim != 2 && dim != 3) || n < 3) return -1;
+  implicit_ell(A, 1, dim, n, ORC_FP64, 0);
+  return 0;
+}
+
 orc_hier* orc_hier_build(int dim, int n, int levels, int variant, int pre, int post, double omega,
                          double base_tol, int base_mode, int base_maxit, int ftz, int fma_, int* err_level) {
+  return orc_hier_build_ex(dim, n, levels, variant, pre, post, omega, base_tol, base_mode, base_maxit, ftz, fma_,
+                           err_level, 0);
+}
+
+orc_hier* orc_hier_build_ex(int dim, int n, int levels, int variant, int pre, int post, double omega,
+                            double base_tol, int base_mode, int base_maxit, int ftz, int fma_, int* err_level,
+                            int implicit) {
   (void)fma_;
   if (err_level) *err_level = -1;
   if (levels < 2 || (n - 1) % (1 << (levels - 1)) != 0 || ((n - 1) >> (levels - 1)) + 1 < 3) return NULL;
@@ -490,6 +628,26 @@ orc_hier* orc_hier_build(int dim, int n, int levels, int variant, int pre, int p
     orc_level* L = &h->lv[l];
     L->prec = variant_prec(variant, l);
     const int nl = ((n - 1) >> (levels - 1 - l)) + 1; /* mesh_fem.hpp:20-22 */
+    if (implicit) {
+      implicit_ell(&L->A, 1, dim, nl, L->prec, ftz);
+      L->n = L->A.rows;
+      double t[27];
+      orc_stencil(dim, nl, t);
+      const double inv = orc_round(1.0 / t[dim == 2 ? 4 : 13], L->prec, ftz); /* multigrid.cpp:296-306 */
+      L->inv_diag = (double*)malloc((size_t)L->n * sizeof(double));
+      for (int64_t r = 0; r < L->n; ++r) L->inv_diag[r] = inv;
+      if (l < levels - 1) {
+        const int nf = ((n - 1) >> (levels - 2 - l)) + 1;
+        implicit_ell(&L->P, 2, dim, nf, L->prec, ftz);
+        implicit_ell(&L->R, 3, dim, nf, L->prec, ftz);
+        L->has_finer = 1;
+      }
+      L->u = (double*)calloc((size_t)L->n, sizeof(double));
+      L->b = (double*)calloc((size_t)L->n, sizeof(double));
+      L->r = (double*)calloc((size_t)L->n, sizeof(double));
+      L->t = (double*)calloc((size_t)L->n, sizeof(double));
+      continue;
+    }
     orc_ell A64;
     orc_stiffness(dim, nl, &A64);
     L->n = A64.rows;
@@ -559,9 +717,9 @@ void orc_jacobi(orc_hier* h, int l, const double* b, double* u, int steps, doubl
  * matrix entries re-rounded on the fly (exact for powers of two) */
 static void transfer_product(const orc_ell* M, const double* x, int prec, double* out, orc_ctx ctx) {
   const int rw = M->rw;
+#pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < M->rows; ++r) {
-    const double* v = M->val + r * rw;
-    const int32_t* c = M->col + r * rw;
+    ELL_ROW(M, r, c, v)
     if (prec == ORC_FP16) {
       double acc = 0.0;
       for (int j = 0; j < rw; ++j) acc = orc_fp16_fma(orc_quantize_fp16(v[j], ctx.ftz), x[c[j]], acc, ctx.ftz, ctx.fma);
@@ -590,6 +748,7 @@ static double restrict_level(const orc_ell* R, const double* r_fine, int fine_pr
     const double nrm = orc_norm2(prod, R->rows);
     if (nrm > 0.0 && isfinite(nrm)) scale = nrm;
   }
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < R->rows; ++i) r_coarse[i] = orc_round(prod[i] / scale, coarse_prec, ctx.ftz);
   free(prod);
   return scale;
@@ -605,6 +764,7 @@ static int prolong_level(const orc_ell* P, const double* c_coarse, int coarse_pr
   if (!(scale > 0.0) || !isfinite(scale)) return -1;
   double* prod = (double*)malloc((size_t)P->rows * sizeof(double));
   transfer_product(P, c_coarse, coarse_prec, prod, ctx);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < P->rows; ++i) c_fine[i] = orc_round(prod[i] * scale, fine_prec, ctx.ftz);
   free(prod);
   return 0;
@@ -702,13 +862,17 @@ double orc_splitmix_double(uint64_t* s) { return (double)(orc_splitmix_next(s) >
 
 /* ir_solver.cpp:21-49 */
 double orc_residual_norm(const orc_ell* A, const double* u, const double* b) {
-  double acc = 0.0;
+  double* rr = (double*)malloc((size_t)A->rows * sizeof(double));
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < A->rows; ++i) {
+    ELL_ROW(A, i, c, v)
     double s = 0.0;
-    for (int j = 0; j < A->rw; ++j) s = fma(A->val[i * A->rw + j], u[A->col[i * A->rw + j]], s);
-    const double r = b[i] - s;
-    acc = fma(r, r, acc);
+    for (int j = 0; j < A->rw; ++j) s = fma(v[j], u[c[j]], s);
+    rr[i] = b[i] - s;
   }
+  double acc = 0.0; /* sequential, in row order */
+  for (int64_t i = 0; i < A->rows; ++i) acc = fma(rr[i], rr[i], acc);
+  free(rr);
   return sqrt(acc);
 }
 

@@ -38,6 +38,15 @@ typedef struct {
   int rw, prec;
   int32_t* col;
   double* val; /* value domain, already rounded to prec */
+  /* implicit operators (col == val == NULL): rows are generated on demand in
+   * exactly the slot order and padding of the assembled ELL (mesh_fem.cpp:
+   * 124-150, 204-295; ell_matrix.cpp:26-28, 90-92), so a 257^3 or larger
+   * level needs no multi-GB slot arrays. gen: 0 explicit, 1 stiffness A,
+   * 2 prolongation P, 3 restriction R; gdim/gn: dimension and the node
+   * count of the row grid (A), or of the FINE grid (P, R); gtaps: the
+   * per-offset coefficients (A: the level stencil, rounded to prec). */
+  int gen, gdim, gn;
+  double gtaps[27];
 } orc_ell;
 
 /* precision.cpp */
@@ -53,6 +62,9 @@ double orc_round(double v, int prec, int ftz);
 /* ell_matrix.cpp */
 int orc_ell_alloc(orc_ell* m, int64_t rows, int64_t cols, int rw, int prec);
 void orc_ell_free(orc_ell* m);
+/* row r of any (explicit or implicit) ELL: rw columns and values */
+void orc_ell_row(const orc_ell* m, int64_t r, int32_t* cols, double* vals);
+void orc_ell_rows(const orc_ell* m, int32_t* cols, double* vals); /* all rows, row-major */
 
 /* kernels.cpp */
 void orc_spmv(const orc_ell* A, const double* x, double* y, orc_ctx ctx);
@@ -66,6 +78,8 @@ double orc_norm2(const double* x, int64_t n);
 /* mesh_fem.cpp */
 int64_t orc_unknowns(int dim, int n);
 int orc_stiffness(int dim, int n, orc_ell* A);
+/* the same operator as an implicit row generator (no slot arrays) */
+int orc_stiffness_implicit(int dim, int n, orc_ell* A);
 int orc_stencil(int dim, int n, double* taps);
 int orc_transfer(int dim, int nf, orc_ell* P, orc_ell* R);
 void orc_rhs(int dim, int n, int k, double* b);
@@ -74,6 +88,11 @@ double orc_nodal_l2(const double* u, const double* v, int64_t len, int dim, int 
 
 /* multigrid.cpp */
 typedef struct orc_hier orc_hier;
+/* implicit = 1: every level operator (A, P, R) is an implicit row generator
+ * (bitwise the assembled ELL, tests/test_oracle.py); 0: assembled ELL */
+orc_hier* orc_hier_build_ex(int dim, int n, int levels, int variant, int pre, int post, double omega,
+                            double base_tol, int base_mode, int base_maxit, int ftz, int fma, int* err_level,
+                            int implicit);
 orc_hier* orc_hier_build(int dim, int n, int levels, int variant, int pre, int post, double omega,
                          double base_tol, int base_mode, int base_maxit, int ftz, int fma, int* err_level);
 void orc_hier_free(orc_hier* h);

@@ -138,6 +138,8 @@ def lib():
     L.mpmg_gpu_update_rc.restype = i; L.mpmg_gpu_update_rc.argtypes = [sp, vp, i32, vp, vp, vp, vp, u32, vp]
     L.mpmg_gpu_update_r.restype = i
     L.mpmg_gpu_update_r.argtypes = [sp, vp, i32, vp, vp, vp, vp, C.c_int64, vp, vp, u32, vp]
+    L.mpmg_gpu_jacobi_slot.restype = i
+    L.mpmg_gpu_jacobi_slot.argtypes = [sp, vp, vp, vp, C.c_int64, vp, d, u32, vp]
     L.mpmg_gpu_update_r_partials.restype = i; L.mpmg_gpu_update_r_partials.argtypes = [i32, i32, i32]
     L.mpmg_gpu_fold.restype = i; L.mpmg_gpu_fold.argtypes = [C.c_int64, vp, vp, C.c_int64, i32, vp, vp, u32, vp]
     L.mpmg_gpu_scale_downcast.restype = i

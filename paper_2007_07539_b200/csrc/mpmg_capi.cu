@@ -103,6 +103,21 @@ int mpmg_gpu_update_r(const mpmg_stencil* A64, const void* c, int32_t c_prec, do
   return rc(e);
 }
 
+int mpmg_gpu_jacobi_slot(const mpmg_stencil* A, const void* b, const void* u_in, void* ring, int64_t ring_len,
+                         const int32_t* slot_dev, double omega, uint32_t policy, void* stream) {
+  if (!valid_stencil(A) || !b || !u_in || !ring || !slot_dev) return MPMG_EINVAL;
+  if (!(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;  // multigrid.cpp:82
+  if (ring_len < (int64_t)mpmg_padded_len(A->dim, A->nodes)) return MPMG_EINVAL;
+  cudaError_t e = cudaSuccess;
+  bool done = false;
+  if (A->prec == MPMG_FP16)
+    done = plane_jacobi_slot_f16(*A, u_in, b, ring, (long long)ring_len, slot_dev, omega, policy, (cudaStream_t)stream, &e);
+  else if (A->prec == MPMG_FP32)
+    done = plane_jacobi_slot_f32(*A, u_in, b, ring, (long long)ring_len, slot_dev, omega, policy, (cudaStream_t)stream, &e);
+  if (!done) return MPMG_EUNSUPPORTED;
+  return rc(e);
+}
+
 int mpmg_gpu_update_r_partials(int32_t dim, int32_t nodes, int32_t c_prec) {
   const int n = plane_update_r_partials(dim, nodes, c_prec);
   return n > 0 ? n : MPMG_EUNSUPPORTED;

@@ -1,0 +1,290 @@
+"""GPU parity at the headline configuration (BASELINE.json configs[1]/[2]):
+3D Poisson 257^3, L = 8 -- the exact kernel instantiations bench.py times
+(pitch 256: the W = 8 binary16 plane kernels for JACOBI / JACOBI_Z / DEFECT,
+the ring-slot Jacobi, UPDATE_R at 4 values per lane, DEFECT64, the 4-wide
+restriction and 8-wide prolongation at Pf = 256; pitch 128 for level 6).
+
+Oracle: the C restatement (oracle/mpmg_oracle.c) with implicit level
+operators (rows generated in the assembled ELL's slot order and padding;
+bitwise the assembled matrices, tests/test_oracle.py), pinned to the
+unmodified reference. Full solves are compared with the reference's own
+257^3 solves (tests/golden/make_golden_257.py -> solves257_*.npz).
+
+Bar: level kernels, V-cycles and outer updates bitwise (binary16/32/64
+values equal; only the sign of an exact zero may differ); ir_solve: same
+iteration count +-1, final residual below the tolerance, solution within
+1e-9 relative L2 of the reference's (on the committed strided sample, plus
+the solution norm).
+"""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import paper_2007_07539_b200 as mg
+from oracle import FP16, FP32, FP64, Oracle
+
+pytestmark = pytest.mark.gpu
+
+O = Oracle()
+DIM, N, L = 3, 257, 8
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def same(a, b):
+    a = np.asarray(a); b = np.asarray(b)
+    return a.shape == b.shape and np.array_equal(a, b, equal_nan=True)
+
+
+def mismatch(a, b):
+    a = np.asarray(a); b = np.asarray(b)
+    bad = ~((a == b) | (np.isnan(a) & np.isnan(b)))
+    idx = np.nonzero(bad)[0]
+    return f"{idx.size} mismatches, first {idx[:5]}: gpu {a[idx[:5]]} oracle {b[idx[:5]]}"
+
+
+def rand_level(rng, n, prec, ftz, scale=1.0):
+    """random values of precision prec (vectorised rounding: cast_vector with scale 1)"""
+    x = (rng.random(n) * 2.0 - 1.0) * scale
+    return O.cast(x, prec, 1.0, O.ctx(ftz))
+
+
+_OH = {}
+
+
+def oracle_h(variant, ftz):
+    key = (variant, ftz)
+    if key not in _OH:
+        _OH.clear()  # one 257^3 oracle hierarchy at a time (~2.5 GB of scratch)
+        _OH[key] = O.hierarchy(DIM, N, L, variant, ftz=ftz, implicit=True)
+    return _OH[key]
+
+
+_RHS = {}
+
+
+def rhs():
+    if "b" not in _RHS:
+        _RHS["b"] = O.rhs(DIM, N)
+    return _RHS["b"]
+
+
+@pytest.fixture(scope="module")
+def rng():
+    return np.random.default_rng(257)
+
+
+# ---- level kernels at pitch 256 (level 7) and 128 (level 6) ---------------
+@pytest.mark.parametrize("variant", ["h_mg", "d_mg"])
+@pytest.mark.parametrize("ftz", [False, True])
+@pytest.mark.parametrize("l", [7, 6])
+def test_level_kernels_257(variant, ftz, l, rng):
+    h = mg.Hierarchy(DIM, N, L, variant, ftz=ftz)
+    ho = oracle_h(variant, ftz)
+    ctx = O.ctx(ftz, True, False)
+    prec = ho.prec(l)
+    Nl = ho.rows(l)
+    A = ho.o.L.orc_level_matrix(ho.h, l, 0).contents
+    u = rand_level(rng, Nl, prec, ftz, 1e-3)  # scaled-residual magnitudes, incl. binary16 subnormals
+    b = rand_level(rng, Nl, prec, ftz, 1.0)
+    y_o = O.spmv_e(A, u, ctx)
+    y_g = h.spmv(l, u)
+    assert same(y_g, y_o), "spmv " + mismatch(y_g, y_o)
+    r_o = O.axpy(prec, -1.0, y_o, b, ctx)
+    r_g = h.defect(l, b, u)
+    assert same(r_g, r_o), "defect " + mismatch(r_g, r_o)
+    j_o = ho.jacobi(l, b, u, 2, ctx=ctx)
+    j_g = h.jacobi(l, b, u, 2)
+    assert same(j_g, j_o), "jacobi " + mismatch(j_g, j_o)
+    z_o = ho.jacobi(l, b, np.zeros(Nl), 3, ctx=ctx)
+    z_g = h.jacobi(l, b, None, 3)  # JACOBI_Z (steps 1+2 fused) + one step
+    assert same(z_g, z_o), "jacobi-from-zero " + mismatch(z_g, z_o)
+    rc_o, _ = ho.restrict(l, b, False, ctx=ctx)
+    rc_g = h.restrict(l, b)
+    assert same(rc_g, rc_o), "restrict " + mismatch(rc_g, rc_o)
+    c = rand_level(rng, ho.rows(l - 1), ho.prec(l - 1), ftz, 0.5)
+    t_o = ho.prolong(l, c, 1.0, ctx=ctx)
+    p_o = O.axpy(prec, 1.0, t_o, u, ctx)
+    p_g = h.prolong_correct(l, c, u)
+    assert same(p_g, p_o), "prolong " + mismatch(p_g, p_o)
+    h.close()
+
+
+# ---- whole V-cycles at 257^3 ------------------------------------------------
+@pytest.mark.parametrize("variant,ftz", [("h_mg", False), ("h_mg", True), ("hsd_mg", False), ("d_mg", False)])
+def test_v_cycle_257(variant, ftz):
+    h = mg.Hierarchy(DIM, N, L, variant, ftz=ftz)
+    ho = oracle_h(variant, ftz)
+    ctx = O.ctx(ftz, True, False)
+    b = rhs()
+    fp = ho.prec(L - 1)
+    rl = O.cast(b, fp, O.norm2(b) if variant != "d_mg" else 1.0, ctx)
+    c_o = ho.v_cycle(rl, ctx)
+    c_g = h.v_cycle(rl)
+    assert same(c_g, c_o), "v_cycle " + mismatch(c_g, c_o)
+    h.close()
+
+
+# ---- outer FP64 kernels through the C ABI, against the oracle ---------------
+def _torch():
+    import torch
+    return torch
+
+
+TDT = {}
+
+
+def tdtype(prec):
+    t = _torch()
+    return {FP16: t.float16, FP32: t.float32, FP64: t.float64}[prec]
+
+
+def to_dev(comp, prec):
+    """compact value-domain array -> padded device vector of precision prec"""
+    t = _torch()
+    Lb = mg.lib()
+    plen = Lb.mpmg_padded_len(DIM, N)
+    out = t.zeros(plen, dtype=tdtype(prec), device="cuda")
+    src = t.from_numpy(np.ascontiguousarray(comp)).to(tdtype(prec)).cuda()
+    mg._check(Lb.mpmg_gpu_pack(DIM, N, prec, src.data_ptr(), out.data_ptr(), None), "pack")
+    return out
+
+
+def from_dev(padded, prec):
+    t = _torch()
+    comp = t.zeros(mg.unknowns(DIM, N), dtype=tdtype(prec), device="cuda")
+    mg._check(mg.lib().mpmg_gpu_unpack(DIM, N, prec, padded.data_ptr(), comp.data_ptr(), None), "unpack")
+    t.cuda.synchronize()
+    return comp.double().cpu().numpy()
+
+
+def dscalar(v):
+    t = _torch()
+    return t.tensor([v], dtype=t.float64, device="cuda")
+
+
+@pytest.mark.parametrize("cprec", [FP16, FP32, FP64])
+@pytest.mark.parametrize("fma", [True, False])
+def test_outer_kernels_257(cprec, fma, rng):
+    """defect_f64 (ir_solver.cpp:92-93, 115-119), update_rc (kernels.cpp:300-341)
+    and its deferred halves update_r + fold, bitwise against the oracle at the
+    headline size (pitch 256)."""
+    t = _torch()
+    Lb = mg.lib()
+    ctx = O.ctx(False, fma, False)
+    pol = mg.policy_word(False, fma, False)
+    A64s = mg.level_stencil(DIM, N, FP64, False)
+    A64 = O.stiffness_implicit(DIM, N)
+    Nn = mg.unknowns(DIM, N)
+    b = rng.random(Nn) * 2 - 1
+    u = rng.random(Nn) * 2 - 1
+    # defect: r = b - A u in FP64 (+ sum-of-squares partials)
+    bd, ud = to_dev(b, FP64), to_dev(u, FP64)
+    rd = t.zeros_like(bd)
+    npart = Lb.mpmg_gpu_partials_len(DIM, N)
+    part = t.zeros(max(npart, 1 << 16), dtype=t.float64, device="cuda")
+    assert Lb.mpmg_gpu_defect_f64(C.byref(A64s), bd.data_ptr(), ud.data_ptr(), rd.data_ptr(), part.data_ptr(),
+                                  None) == 0
+    r_o = O.axpy(FP64, -1.0, O.spmv_e(A64, u, ctx), b, ctx)
+    r_g = from_dev(rd, FP64)
+    assert same(r_g, r_o), "defect_f64 " + mismatch(r_g, r_o)
+    # fused update: u += a c; r -= a A c
+    c = rand_level(rng, Nn, cprec, False, 1.0)
+    alpha = 3.7e-3
+    cd, ad = to_dev(c, cprec), dscalar(alpha)
+    r1, u1 = rd.clone(), ud.clone()
+    assert Lb.mpmg_gpu_update_rc(C.byref(A64s), cd.data_ptr(), cprec, r1.data_ptr(), u1.data_ptr(), ad.data_ptr(),
+                                 part.data_ptr(), pol, None) == 0
+    ro, uo = O.update_rc_e(A64, r_o, u, c, alpha, ctx)
+    rg, ug = from_dev(r1, FP64), from_dev(u1, FP64)
+    assert same(rg, ro), "update_rc r " + mismatch(rg, ro)
+    assert same(ug, uo), "update_rc u " + mismatch(ug, uo)
+    if cprec == FP64:
+        return  # the deferred form exists for binary16/32 finest levels only
+    # deferred halves over two iterations: update_r (+ ring slot), then fold
+    plen = Lb.mpmg_padded_len(DIM, N)
+    ring_len = (plen + 63) // 64 * 64
+    ring = t.zeros(2 * ring_len, dtype=tdtype(cprec), device="cuda")
+    scales = t.zeros(2, dtype=t.float64, device="cuda")
+    c2 = rand_level(rng, Nn, cprec, False, 1e-3)
+    alphas = [alpha, 2.5e-5]
+    p2 = t.zeros(max(npart, Lb.mpmg_gpu_update_r_partials(DIM, N, cprec)), dtype=t.float64, device="cuda")
+    r2, u2 = rd.clone(), ud.clone()
+    ro2, uo2 = r_o, u
+    for k, (cc, a) in enumerate(zip((c, c2), alphas)):
+        slot = t.tensor([k], dtype=t.int32, device="cuda")
+        ccd = to_dev(cc, cprec)
+        assert Lb.mpmg_gpu_update_r(C.byref(A64s), ccd.data_ptr(), cprec, r2.data_ptr(), dscalar(a).data_ptr(),
+                                    p2.data_ptr(), ring.data_ptr(), ring_len, slot.data_ptr(), scales.data_ptr(),
+                                    pol, None) == 0
+        ro2, uo2 = O.update_rc_e(A64, ro2, uo2, cc, a, ctx)
+    cnt = t.tensor([2], dtype=t.int32, device="cuda")
+    assert Lb.mpmg_gpu_fold(plen, u2.data_ptr(), ring.data_ptr(), ring_len, cprec, scales.data_ptr(),
+                            cnt.data_ptr(), pol, None) == 0
+    rg2, ug2 = from_dev(r2, FP64), from_dev(u2, FP64)
+    assert same(rg2, ro2), "update_r " + mismatch(rg2, ro2)
+    assert same(ug2, uo2), "fold " + mismatch(ug2, uo2)
+
+
+@pytest.mark.parametrize("ftz", [False, True])
+def test_jacobi_into_ring_slot_257(ftz, rng):
+    """The last finest post-smoothing step of a deferred-correction cycle,
+    written straight into a ring slot (the OPT-bit-2 plane kernel), bitwise one
+    jacobi_smooth step (multigrid.cpp:79-89)."""
+    t = _torch()
+    Lb = mg.lib()
+    ho = oracle_h("h_mg", ftz)
+    ctx = O.ctx(ftz, True, False)
+    A16 = mg.level_stencil(DIM, N, FP16, ftz)
+    Nn = mg.unknowns(DIM, N)
+    b = rand_level(rng, Nn, FP16, ftz, 1.0)
+    u = rand_level(rng, Nn, FP16, ftz, 1e-2)
+    plen = Lb.mpmg_padded_len(DIM, N)
+    ring_len = (plen + 63) // 64 * 64
+    ring = t.full((3 * ring_len,), float("nan"), dtype=t.float16, device="cuda")
+    slot = t.tensor([2], dtype=t.int32, device="cuda")
+    bd, ud = to_dev(b, FP16), to_dev(u, FP16)
+    ring[2 * ring_len: 2 * ring_len + plen].zero_()  # ghosts of the slot are zero (as allocated by the solver)
+    assert Lb.mpmg_gpu_jacobi_slot(C.byref(A16), bd.data_ptr(), ud.data_ptr(), ring.data_ptr(), ring_len,
+                                   slot.data_ptr(), 2.0 / 3.0, mg.policy_word(ftz), None) == 0
+    j_g = from_dev(ring[2 * ring_len:2 * ring_len + plen].contiguous(), FP16)
+    j_o = ho.jacobi(L - 1, b, u, 1, ctx=ctx)
+    assert same(j_g, j_o), "jacobi->slot " + mismatch(j_g, j_o)
+    assert t.isnan(ring[:2 * ring_len]).all(), "wrote outside its slot"
+
+
+# ---- full solves against the reference's own 257^3 runs -------------------
+def golden(variant, ftz):
+    path = os.path.join(GOLDEN, f"solves257_{variant}" + ("_ftz1" if ftz else "") + ".npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{os.path.basename(path)} not generated")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("variant,ftz", [("h_mg", False), ("d_mg", False), ("hsd_mg", False), ("h_mg", True)])
+def test_ir_solve_257(variant, ftz):
+    g = golden(variant, ftz)
+    key = f"{variant}_ftz{int(ftz)}"
+    its_ref = int(g[f"{key}_meta"][0])
+    hist_ref = g[f"{key}_history"]
+    stride = int(g["stride"])
+    b = mg.problem_rhs(DIM, N)
+    tol = 1e-10 * float(np.sqrt(np.dot(b, b)))
+    h = mg.Hierarchy(DIM, N, L, variant, ftz=ftz)
+    u, rep = h.ir_solve(b, mg.IrConfig(outer_tolerance=tol))
+    h.close()
+    assert rep.converged and bool(g[f"{key}_meta"][1])
+    assert abs(rep.iterations - its_ref) <= 1, (rep.iterations, its_ref)
+    assert rep.final_residual < tol
+    # the first residual is ||b|| (u0 = 0) up to the reduction order
+    assert rep.residual_history[0] == pytest.approx(hist_ref[0], rel=1e-13)
+    # the trajectory: the same contraction per iteration (a few digits while
+    # far above the rounding level)
+    k = min(len(hist_ref), len(rep.residual_history), 4)
+    np.testing.assert_allclose(rep.residual_history[:k], hist_ref[:k], rtol=1e-3)
+    us, ur = u[::stride], g[f"{key}_u_sample"]
+    rel = np.linalg.norm(us - ur) / np.linalg.norm(ur)
+    assert rel <= 1e-9, rel
+    un = float(np.sqrt(np.dot(u, u)))
+    assert un == pytest.approx(float(g[f"{key}_u_norm"]), rel=1e-9)

@@ -385,3 +385,42 @@ def test_ir_solve_golden(name):  # ir_solver.cpp:51-127
     assert s["final_residual"] == float(g[f"{name}_final"])
     if f"{name}_u" in g:
         assert same_bits(s["u"], g[f"{name}_u"])
+
+
+@pytest.mark.parametrize("dim,n,L", [(2, 17, 4), (3, 9, 3), (3, 17, 4), (2, 33, 5)])
+@pytest.mark.parametrize("variant", ["d_mg", "h_mg", "hsd_mg", "dsh_mg"])
+@pytest.mark.parametrize("ftz", [0, 1])
+def test_implicit_operators_equal_assembled(dim, n, L, variant, ftz):
+    """The oracle's implicit level operators (rows generated on demand, used
+    at 257^3 where the assembled ELL is GBs) are the assembled ELL matrices
+    row for row -- columns, values and padding -- and give bitwise the same
+    V-cycle (mesh_fem.cpp:124-150, 204-295; ell_matrix.cpp:90-92)."""
+    he = O.hierarchy(dim, n, L, variant, ftz=ftz)
+    hi = O.hierarchy(dim, n, L, variant, ftz=ftz, implicit=True)
+    for l in range(L):
+        assert same_bits(he.invdiag(l), hi.invdiag(l))
+        for which in (0, 1, 2):
+            a, b = he.matrix(l, which), hi.matrix(l, which)
+            if a is None:
+                assert b is None
+                continue
+            assert np.array_equal(a[0], b[0]) and same_bits(a[1], b[1]), (l, which)
+    b = O.rhs(dim, n)
+    ctx = O.ctx(ftz)
+    rl = O.cast(b, he.prec(L - 1), O.norm2(b) if variant != "d_mg" else 1.0, ctx)
+    assert same_bits(he.v_cycle(rl, ctx), hi.v_cycle(rl, ctx))
+    A = O.stiffness(dim, n)
+    Ai = O.stiffness_implicit(dim, n)
+    u = np.random.default_rng(3).random(len(b))
+    assert same_bits(O.spmv(A[0], A[1], FP64, u), O.spmv_e(Ai, u))
+    assert O.L.orc_residual_norm(Ai, u, b) == O.residual_norm_e(Ai, u, b)
+
+
+def test_implicit_ir_solve_equals_assembled():
+    ho = O.hierarchy(3, 33, 5, "h_mg", ftz=False)
+    hi = O.hierarchy(3, 33, 5, "h_mg", ftz=False, implicit=True)
+    b = O.rhs(3, 33)
+    s1 = ho.ir_solve(b, ctx=O.ctx(False))
+    s2 = hi.ir_solve(b, ctx=O.ctx(False))
+    assert s1["iterations"] == s2["iterations"]
+    assert same_bits(s1["history"], s2["history"]) and same_bits(s1["u"], s2["u"])
