@@ -186,7 +186,8 @@ def test_outer_kernels_257(cprec, fma, rng):
     part = t.zeros(max(npart, 1 << 16), dtype=t.float64, device="cuda")
     assert Lb.mpmg_gpu_defect_f64(C.byref(A64s), bd.data_ptr(), ud.data_ptr(), rd.data_ptr(), part.data_ptr(),
                                   None) == 0
-    r_o = O.axpy(FP64, -1.0, O.spmv_e(A64, u, ctx), b, ctx)
+    fctx = O.ctx(False, True, False)  # mpmg_gpu_defect_f64 is the FMA-policy defect (the solver's default)
+    r_o = O.axpy(FP64, -1.0, O.spmv_e(A64, u, fctx), b, fctx)
     r_g = from_dev(rd, FP64)
     assert same(r_g, r_o), "defect_f64 " + mismatch(r_g, r_o)
     # fused update: u += a c; r -= a A c
