@@ -17,8 +17,10 @@ grid is 133 MB and the three of them exceed the 126 MB L2; the L2 is
 additionally flushed (a 512 MiB write) before every timed solve.
 
 `--impl reference` times the reference's own CPU implementation (the
-unmodified library compiled from /root/reference into oracle/_ref/) on a
-bounded sample of the same workload: see cpu_reference() below.
+unmodified library compiled from /root/reference into oracle/_ref/) on the
+same workload: one complete 257^3 solve (~10 minutes on one core), see
+run_reference(). The B200 arm's `cpu_baseline` is a bounded, measured sample
+(one complete reference solve at 65^3): see cpu_reference().
 """
 from __future__ import annotations
 
@@ -283,7 +285,7 @@ def run_b200(a):
     out["clocks"] = clocks
     if not a.no_cpu and ws == 1:
         try:
-            out["cpu_baseline"] = cpu_reference(a, dim, n, L, ftz, mix["iterations"], steps=1)
+            out["cpu_baseline"] = cpu_reference(a, dim, n, L, ftz)
         except Exception as ex:  # reported, not fatal
             out["cpu_baseline"] = {"error": str(ex)[:200]}
     print(json.dumps(out), flush=True)
@@ -422,42 +424,58 @@ def kernel_roofline(a, dim, n, L, ftz, dev, flush_l2):
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref: the unmodified reference library)
 # ---------------------------------------------------------------------------
-CPU_SAMPLE_NODES = 129   # 127^3 = 2,048,383 unknowns, L = 7
-CPU_SAMPLE_ITS = 2
-# outer-iteration counts the reference itself needs at 257^3, u0 = 0, tol
-# 1e-10||b|| (measured by running the reference)
-REF_ITS_257 = {("h_mg", False): 10, ("d_mg", False): 7, ("d_mg", True): 7}
+CPU_SAMPLE_NODES = 65  # the my-arm cpu_baseline sample: a complete solve at 65^3
 
 
-def cpu_reference(a, dim, n, L, ftz, gpu_iterations, steps=1):
-    """Times the reference's ir_solve on the host (single-threaded library,
-    1 core) on a bounded sample: the same variant/policy/smoother at 129^3
-    (L=7), CPU_SAMPLE_ITS outer iterations (hierarchy build excluded, as in
-    the reference's own SolveReport.wall_time_s). Scaled to the workload:
-    seconds/iteration x (N_257 / N_129) x iterations the reference needs at
-    257^3 (falls back to the GPU's count when no reference count is pinned)."""
+def host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def reference_solve(a, dim, n, L, ftz):
+    """One complete reference ir_solve (ir_solver.cpp:51-127) of the variant /
+    policy / smoother in `a` on a dim-D n-node grid: the unmodified library
+    (oracle/_ref), single-threaded (1 core). The time is the reference's own
+    SolveReport.wall_time_s (steady_clock around the solve, ir_solver.cpp:61,
+    124-125); the hierarchy build is reported separately."""
     from oracle import Reference
     R = Reference()
-    sn = CPU_SAMPLE_NODES if n > CPU_SAMPLE_NODES else n
+    hr = R.hierarchy(dim, n, L, a.variant, pre=a.pre, post=a.post, ftz=ftz)
+    res = hr.ir_solve(rel_tol=a.rel_tol, want_u=False)
+    return res, hr.build_seconds
+
+
+def cpu_reference(a, dim, n, L, ftz):
+    """cpu_baseline of the B200 arm: a bounded sample -- one COMPLETE reference
+    solve of the same variant, policy and smoother on the 65^3 grid (about
+    10 s on one core; not scaled to 257^3). The full-size reference solve is
+    the --impl reference arm."""
+    sn = min(n, CPU_SAMPLE_NODES)
     sL = max_depth(sn)
-    hr = R.hierarchy(dim, sn, sL, a.variant, pre=a.pre, post=a.post, ftz=ftz)
-    walls = []
-    for _ in range(steps):
-        res = hr.ir_solve(rel_tol=a.rel_tol, max_it=CPU_SAMPLE_ITS, want_u=False)
-        walls.append(res["wall_s"])
-    per_it = min(walls) / max(1, res["iterations"])
-    Ns = (sn - 2) ** dim
-    Nf = (n - 2) ** dim
-    its = REF_ITS_257.get((a.variant, ftz), gpu_iterations) if n == 257 else gpu_iterations
-    value = per_it * (Nf / Ns) * its
-    return {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
-            "sample": f"reference ir_solve (oracle/_ref, unmodified library) at {sn}^{dim} L={sL}, "
-                      f"{res['iterations']} outer its, {per_it:.3f} s/it; x{Nf / Ns:.3f} unknowns x {its} its "
-                      f"(reference count at {n}^{dim})",
-            "sample_wall_s": sum(walls), "build_s": hr.build_seconds}
+    t0 = time.perf_counter()
+    res, build_s = reference_solve(a, dim, sn, sL, ftz)
+    return {"value": res["wall_s"], "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"one complete reference ir_solve (oracle/_ref, unmodified library, 1 thread) at {sn}^{dim} "
+                      f"L={sL}, {a.variant.upper()}, same policy and smoother: {res['iterations']} outer its; "
+                      f"measured, not scaled to {n}^{dim} (the --impl reference arm runs {n}^{dim})",
+            "measured_config": f"{sn}^{dim}", "iterations": res["iterations"], "converged": res["converged"],
+            "build_s": build_s, "sample_wall_s": time.perf_counter() - t0, **host_info()}
 
 
 def run_reference(a):
+    """--impl reference: the reference's own CPU solver at the SAME workload
+    as the B200 arm (3D 257^3, L = 8, V(3,3), the same variant and policy),
+    one complete solve. The reference is single-threaded and one solve takes
+    ~10 minutes on one core, so exactly one timed solve runs regardless of
+    --steps/--warmup (reported as steps = 1, warmup = 0)."""
     ws, rank, _ = dist_info()
     if ws > 1 and rank != 0:
         return  # rank 0 alone runs the CPU reference
@@ -469,22 +487,22 @@ def run_reference(a):
     except Exception as ex:
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {ex}"[:200]}))
         return
-    vals = []
     t0 = time.perf_counter()
-    for i in range(a.warmup + a.steps):
-        cb = cpu_reference(a, a.dim, a.nodes, L, ftz, REF_ITS_257.get((a.variant, ftz), 10), steps=1)
-        if i >= a.warmup:
-            vals.append(cb["value"])
-    v = sum(vals) / len(vals)
+    res, build_s = reference_solve(a, a.dim, a.nodes, L, ftz)
+    v = res["wall_s"]
     N = (a.nodes - 2) ** a.dim
-    cb["value"] = v
-    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
-           "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "fp16 (software-emulated)" if a.variant == "h_mg" else "fp64",
-           "data": "synthetic: the reference's manufactured Poisson problem",
+    cb = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
+          "sample": f"one complete reference ir_solve at the stated config ({a.nodes}^{a.dim}, L={L}); "
+                    f"SolveReport.wall_time_s, hierarchy build excluded", "build_s": build_s, **host_info()}
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": 1,
+           "warmup": 0, "requested": {"steps": a.steps, "warmup": a.warmup}, "ms_per_step": v * 1e3,
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+           "dtype": "fp16 (software-emulated)" if a.variant == "h_mg" else ("fp64" if a.variant == "d_mg" else "mixed"),
+           "data": "synthetic: the reference's manufactured Poisson problem (assemble_rhs k=1), u0 = 0",
            "config": {"workload": f"{a.dim}D Poisson {a.nodes}^{a.dim} ({N} unknowns), L={L}, V({a.pre},{a.post}),"
                                   f" {a.variant.upper()} IR to {a.rel_tol:g}*||b||", "variant": a.variant,
                       "policy": {"flush_subnormals_to_zero": ftz, "fused_multiply_add": True}},
+           "iterations": res["iterations"], "converged": res["converged"], "final_residual": res["final_residual"],
            "cpu_baseline": cb,
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "wall_s": time.perf_counter() - t0}
