@@ -246,6 +246,11 @@ int mpmg_gpu_cast(int64_t n, const void* x, int32_t x_prec, void* out, int32_t o
                   double scale, uint32_t policy, void* stream);
 /* dot_fp64 / norm2_fp64 (kernels.cpp:368-395): sequential fma accumulation in
  * index order on one device thread -- bitwise the reference's value. */
+/* Validate mode (ExecContext::validate; kernels.cpp:90-113 validate_finite,
+ * multigrid.cpp:259-265): *index = the smallest i with x[i] non-finite (NaN
+ * or +-inf; binary16: exponent field all ones), or -1. Synchronous on
+ * `stream` (the result is a host value). */
+int mpmg_gpu_find_nonfinite(int64_t n, const void* x, int32_t x_prec, int64_t* index, void* stream);
 int mpmg_gpu_dot_seq(int64_t n, const void* x, int32_t x_prec, const void* y, int32_t y_prec, double* out_dev,
                      int32_t take_sqrt, void* stream);
 

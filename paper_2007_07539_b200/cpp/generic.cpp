@@ -3,12 +3,23 @@
 
 #include <cmath>
 #include <stdexcept>
+#include <string>
+
+#include "mpmg/errors.hpp"
 
 namespace mpmg::detail {
 
 namespace {
 std::uint64_t vb(Precision p) { return static_cast<std::uint64_t>(bytes_per_value(p)); }
 }  // namespace
+
+// validate mode: the reference's validate_finite (kernels.cpp:90-113) on a
+// device vector -- the first non-finite index, found on the device
+void dev_validate(const DevVec& v, const char* what) {
+  int64_t idx = -1;
+  check(mpmg_gpu_find_nonfinite(static_cast<int64_t>(v.n), v.get(), prec_code(v.prec), &idx, nullptr), what);
+  if (idx >= 0) throw ValidationError(std::string(what) + ": non-finite entry at index " + std::to_string(idx));
+}
 
 void dev_spmv(const EllMatrix& A, const DevVec& x, DevVec& y, const ExecContext& ctx) {
   const DeviceEll& D = A.device();
@@ -17,6 +28,7 @@ void dev_spmv(const EllMatrix& A, const DevVec& x, DevVec& y, const ExecContext&
         "spmv");
   const std::uint64_t slots = A.rows() * static_cast<std::uint64_t>(A.row_width());
   add(ctx.traffic, slots * vb(x.prec) * 2, A.rows() * vb(y.prec), slots * 4, slots * 2);
+  if (ctx.validate) dev_validate(y, "spmv");  // kernels.cpp:254
 }
 
 void dev_axpy(double alpha, const DevVec& x, const DevVec& y, DevVec& out, const ExecContext& ctx) {
@@ -24,6 +36,7 @@ void dev_axpy(double alpha, const DevVec& x, const DevVec& y, DevVec& out, const
                       policy_word(ctx), nullptr),
         "axpy");
   add(ctx.traffic, 2 * x.n * vb(x.prec), x.n * vb(x.prec), 0, 2 * x.n);
+  if (ctx.validate) dev_validate(out, "axpy");  // kernels.cpp:273
 }
 
 void dev_vmul(const DevVec& a, const DevVec& b, DevVec& out, const ExecContext& ctx) {
@@ -31,6 +44,7 @@ void dev_vmul(const DevVec& a, const DevVec& b, DevVec& out, const ExecContext& 
                               policy_word(ctx), nullptr),
         "vec_multiply");
   add(ctx.traffic, 2 * a.n * vb(a.prec), a.n * vb(a.prec), 0, a.n);
+  if (ctx.validate) dev_validate(out, "vec_multiply");  // kernels.cpp:291
 }
 
 static double seq(const DevVec& x, const DevVec& y, int take_sqrt) {
@@ -140,6 +154,7 @@ double dev_restrict(const EllMatrix& R, const DevVec& r_fine, DevVec& r_coarse, 
           "restrict");
   }
   add(ctx.traffic, 0, R.rows() * vb(r_coarse.prec), 0, R.rows());
+  if (ctx.validate) dev_validate(r_coarse, "restrict_with_cast");  // multigrid.cpp:259-265
   return scale;
 }
 

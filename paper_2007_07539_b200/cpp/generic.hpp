@@ -11,6 +11,8 @@
 
 namespace mpmg::detail {
 
+// validate mode: throws ValidationError("<what>: non-finite entry at index i")
+void dev_validate(const DevVec& v, const char* what);
 // y = A x, r = b - A u etc. on device vectors of matching precision
 void dev_spmv(const EllMatrix& A, const DevVec& x, DevVec& y, const ExecContext& ctx);
 void dev_axpy(double alpha, const DevVec& x, const DevVec& y, DevVec& out, const ExecContext& ctx);

@@ -73,7 +73,10 @@ IrResult ir_solve(const EllMatrix& A_high, const PVector& b_high, MgHierarchy& h
   const bool scale_enabled = scale_on(config, h);
 
   const auto& tag = A_high.stencil_tag();
-  const bool fast = h.spec() && tag.dim == h.spec()->dim && tag.nodes == h.spec()->finest_nodes_per_dim;
+  // validate mode checks every kernel's output (kernels.cpp:96-113): it runs
+  // op for op on the generic device path, which checks each result
+  const bool fast = !caller_ctx.validate && h.spec() && tag.dim == h.spec()->dim &&
+                    tag.nodes == h.spec()->finest_nodes_per_dim;
   if (fast) {
     auto* s = static_cast<mpmg_solver*>(h.device_solver(caller_ctx));
     mpmg_solve_params p{};
@@ -151,6 +154,10 @@ IrResult ir_solve(const EllMatrix& A_high, const PVector& b_high, MgHierarchy& h
                                  static_cast<double*>(r.get()), static_cast<double*>(u.get()), al.as<double>(),
                                  policy_word(ctx), nullptr),
           "update_residuum_correction");
+    if (ctx.validate) {  // kernels.cpp:337-340
+      dev_validate(r, "update_residuum_correction");
+      dev_validate(u, "update_residuum_correction");
+    }
     const std::uint64_t slots = n * static_cast<std::uint64_t>(A_high.row_width());
     add(ctx.traffic, slots * 8 + 2 * n * 8 + n * static_cast<std::uint64_t>(bytes_per_value(mg)), 2 * n * 8, slots * 4,
         2 * slots + 4 * n);

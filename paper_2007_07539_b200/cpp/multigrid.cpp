@@ -9,8 +9,10 @@
 //    order (multigrid.cpp:79-393).
 #include "mpmg/multigrid.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <stdexcept>
+#include <vector>
 #include <string>
 #include <utility>
 
@@ -131,17 +133,22 @@ MgHierarchy MgHierarchy::build(const ProblemSpec& spec, MgVariant variant, const
     g.precision = vc.level_precision[static_cast<std::size_t>(l)];
     const StructuredGrid grid{spec.dim, spec.nodes_at_level(l)};
     const EllMatrix A64 = assemble_stiffness(grid);
-    // inverse of the assembled diagonal (multigrid.cpp:296-306)
-    PVector inv(A64.rows(), Precision::FP64);
-    for (std::size_t row = 0; row < A64.rows(); ++row) {
-      double diag = 0.0;
-      for (int s = 0; s < A64.row_width(); ++s)
-        if (A64.col(row, s) == static_cast<std::int32_t>(row)) { diag = A64.value(row, s); break; }
-      inv.set(row, 1.0 / diag);
-    }
+    // inverse of the assembled diagonal (multigrid.cpp:296-306), cast to the
+    // level precision. Every row of the generated operator carries the same
+    // diagonal coefficient, so it is read from one row (the slot whose column
+    // is the row itself) and broadcast.
+    std::vector<std::int32_t> cols(static_cast<std::size_t>(A64.row_width()));
+    std::vector<double> vals(cols.size());
+    A64.row(0, cols.data(), vals.data());
+    double diag = 0.0;
+    for (std::size_t s = 0; s < cols.size(); ++s)
+      if (cols[s] == 0) { diag = vals[s]; break; }
+    PVector d(A64.rows(), g.precision);
+    d.set(0, 1.0 / diag, policy);
+    if (g.precision == Precision::FP16) std::fill(d.f16().begin(), d.f16().end(), d.f16()[0]);
+    else if (g.precision == Precision::FP32) std::fill(d.f32().begin(), d.f32().end(), d.f32()[0]);
+    else std::fill(d.f64().begin(), d.f64().end(), d.f64()[0]);
     g.A = cast_checked(A64, g.precision, policy, l);
-    PVector d(inv.size(), g.precision);
-    for (std::size_t i = 0; i < inv.size(); ++i) d.set(i, inv.get(i), policy);
     g.inv_diag = std::move(d);
     if (l < spec.levels - 1) {
       auto [P, R] = assemble_transfer(StructuredGrid{spec.dim, spec.nodes_at_level(l + 1)}, grid);
@@ -225,8 +232,9 @@ void MgHierarchy::v_cycle(const PVector& b, PVector& c, const ExecContext& ctx) 
   require(c.precision() == finest_precision(), "v_cycle: output precision mismatch");
   require(b.size() == levels_.back().unknowns(), "v_cycle: dimension mismatch");
   require(c.size() == levels_.back().unknowns(), "v_cycle: output dimension mismatch");
-  if (solvers_) {
-    // the fused stencil V-cycle on the device (values exchanged as binary64)
+  if (solvers_ && !ctx.validate) {
+    // the fused stencil V-cycle on the device (values exchanged as binary64);
+    // validate mode runs op for op (every kernel's output checked)
     auto* s = static_cast<mpmg_solver*>(device_solver(ctx));
     std::vector<double> bb(b.size()), cc(c.size());
     for (std::size_t i = 0; i < b.size(); ++i) bb[i] = b.get(i);

@@ -171,6 +171,20 @@ __global__ void k_dot_seq(long long n, const void* x, const void* y, double* out
   *out = sqrt_it ? sqrt(acc) : acc;
 }
 
+// validate mode (kernels.cpp:90-113, multigrid.cpp:259-265): the smallest
+// index holding a non-finite value (binary16: exponent field all ones), or
+// n when every entry is finite
+template <int XP>
+__global__ void k_find_nonfinite(long long n, const void* x, unsigned long long* first) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool bad;
+  if constexpr (XP == P16) bad = (__half_as_ushort(static_cast<const __half*>(x)[i]) & 0x7C00u) == 0x7C00u;
+  else if constexpr (XP == P32) bad = !isfinite(static_cast<const float*>(x)[i]);
+  else bad = !isfinite(static_cast<const double*>(x)[i]);
+  if (bad) atomicMin(first, (unsigned long long)i);
+}
+
 template <typename F>
 cudaError_t by_prec(int p, F&& f) {
   switch (p) {
@@ -303,6 +317,32 @@ int mpmg_gpu_dot_seq(int64_t n, const void* x, int32_t x_prec, const void* y, in
       return cudaGetLastError();
     });
   }));
+}
+
+int mpmg_gpu_find_nonfinite(int64_t n, const void* x, int32_t x_prec, int64_t* index, void* stream) {
+  if (n < 0 || !x || !vp(x_prec) || !index) return MPMG_EINVAL;
+  *index = -1;
+  if (n == 0) return MPMG_OK;
+  const cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, 8, s);
+  const unsigned long long init = (unsigned long long)n;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, &init, 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = by_prec(x_prec, [&](auto xp) -> cudaError_t {
+      k_find_nonfinite<decltype(xp)::value><<<nb(n), kT, 0, s>>>(n, x, d);
+      return cudaGetLastError();
+    });
+  unsigned long long first = init;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&first, d, 8, cudaMemcpyDeviceToHost, s);
+  if (d) {
+    const cudaError_t ef = cudaFreeAsync(d, s);
+    if (e == cudaSuccess) e = ef;
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return rc(e);
+  *index = first < init ? (int64_t)first : -1;
+  return MPMG_OK;
 }
 
 }  // extern "C"

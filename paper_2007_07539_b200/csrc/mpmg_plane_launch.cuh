@@ -119,13 +119,19 @@ struct PlaneLaunch {
   using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
   static constexpr auto kernel = k_plane<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
 
-  // grid: y-tiles x z-chunks, z-chunks sized so the grid is about one wave
+  // grid: y-tiles x z-chunks, z-chunks sized so the grid is about one wave.
+  // The wave is that of the FTZ-off/FMA-on build for every policy, so the
+  // grid -- and the number of norm partials the FP64-epilogue ops write --
+  // does not depend on the policy's register footprint (k_control sums
+  // exactly the count mpmg_solver_create sized).
   static dim3 grid(int* zc, int pz = P) {
     static int per_sm = -1;
     if (per_sm < 0) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem);
+      constexpr auto ref = k_plane<LP, CP, EP, OP, false, true, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
+      cudaFuncSetAttribute(ref, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem);
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, K::kThreads, K::kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ref, K::kThreads, K::kSmem);
       per_sm = n > 0 ? n : 1;
     }
     const int ytiles = (P - 1 + K::TY - 1) / K::TY;

@@ -473,7 +473,7 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
   if (!cfg) return fail(MPMG_EINVAL, -1);
   const mpmg_solver_config c = *cfg;
   // ProblemSpec::validate (mesh_fem.cpp:57-69) + build preconditions (multigrid.cpp:285-286)
-  if ((c.dim != 2 && c.dim != 3) || c.k < 1 || c.levels < 2 || c.nodes < 3 ||
+  if ((c.dim != 2 && c.dim != 3) || c.k < 1 || c.levels < 2 || c.levels > 30 || c.nodes < 3 ||
       (c.nodes - 1) % (1 << (c.levels - 1)) != 0 || ((c.nodes - 1) >> (c.levels - 1)) + 1 < 3) {
     last_error() = "invalid ProblemSpec";
     return fail(MPMG_EINVAL, -1);
@@ -482,7 +482,6 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
     last_error() = "invalid smoother/base-solver config";
     return fail(MPMG_EINVAL, -1);
   }
-  if (c.levels > 30) return fail(MPMG_EINVAL, -1);
   cudaError_t e = cudaSetDevice(c.device);
   if (e != cudaSuccess) { set_cuda_error(e); return fail(MPMG_ECUDA, -1); }
   auto* S = new mpmg_solver();
@@ -627,8 +626,19 @@ int mpmg_solver_solve_device(mpmg_solver* S, const double* b_dev, double* u_dev,
                              double* hist, int32_t hist_cap, mpmg_solve_report* rep) {
   if (!S || !pp || !(pp->outer_tolerance > 0.0) || pp->max_outer_iterations < 0) return MPMG_EINVAL;
   const mpmg_solve_params p = *pp;
-  if (p.max_outer_iterations + 1 > S->hist_cap) return MPMG_EINVAL;
   cudaStream_t q = S->s;
+  if (p.max_outer_iterations + 1 > S->hist_cap) {  // history sized per solve (any max_outer_iterations)
+    cudaError_t ea = cudaStreamSynchronize(q);
+    if (ea == cudaSuccess) {
+      S->allocs.erase(std::remove(S->allocs.begin(), S->allocs.end(), (void*)S->hist), S->allocs.end());
+      ea = cudaFree(S->hist);
+      S->hist = nullptr;
+    }
+    if (ea == cudaSuccess) ea = S->alloc(&S->hist, (size_t)(p.max_outer_iterations + 1) * 8);
+    if (ea != cudaSuccess) return finish(ea);
+    S->hist_cap = p.max_outer_iterations + 1;
+    S->gvalid = false;  // the graph captured the old history pointer
+  }
   const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaSuccess;
   if (b_dev && b_dev != S->b) e = cudaMemcpyAsync(S->b, b_dev, S->len * 8, cudaMemcpyDeviceToDevice, q);

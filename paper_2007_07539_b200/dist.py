@@ -60,6 +60,15 @@ class SlabPlan:
         self.agg = max(l for l in range(levels) if not self.dist[l]) if not all(self.dist) else -1
         if self.agg < 0:
             raise ValueError("no coarse level left for the agglomerated solve")
+        # the agglomeration level is restricted into slab-wise too: its planes
+        # must split evenly, or coarse planes would be left out (and the last
+        # rank's prolongation would read past its slab)
+        if self.P[self.agg] % world != 0:
+            raise ValueError(f"agglomeration pitch {self.P[self.agg]} is not divisible by {world} ranks")
+        try:
+            self.check()
+        except AssertionError as ex:
+            raise ValueError(f"invalid slab decomposition: {ex}") from None
 
     def nodes_at(self, l):
         return self.P[l] + 1
@@ -83,7 +92,7 @@ class SlabPlan:
             cover = []
             for r in range(self.world):
                 s = self.slab(l, r)
-                assert s.nz >= 1
+                assert s.nz >= (1 if l > self.agg else 0)  # an agglomeration slab may be empty
                 cover.extend(range(s.z_lo, s.z_lo + s.nz))
             assert cover == list(range(1, self.P[l])), (l, cover[:5])
             if l > self.agg:

@@ -6,6 +6,7 @@
 //   built + run by tests/test_cpp_api.py
 #include <cmath>
 #include <cstdio>
+#include <limits>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -247,6 +248,49 @@ static void solves() {
     CHECK(values_equal(c1, c2));
     std::printf("H_MG 33^3: fused %d its, generic %d its, rel diff %.2e\n", fast.report.iterations,
                 gen.report.iterations, std::sqrt(num / den));
+  }
+  // validate mode (ExecContext::validate; kernels.cpp:96-113, multigrid.cpp:
+  // 259-265, 365-369): the fused path hands over to the op-for-op path,
+  // which checks every kernel output on the device
+  {
+    const ProblemSpec spec{3, 1, 33, 5};
+    const Problem p = build_problem(spec);
+    ExecContext ctx;
+    ctx.policy.flush_subnormals_to_zero = false;
+    MgHierarchy h = MgHierarchy::build(spec, MgVariant::H_MG, {}, {}, ctx.policy);
+    IrConfig cfg;
+    cfg.outer_tolerance = 1e-10 * norm2_fp64(p.b, {});
+    const IrResult fast = ir_solve(p.A, p.b, h, cfg, ctx);
+    ExecContext vctx = ctx;
+    vctx.validate = true;
+    const IrResult val = ir_solve(p.A, p.b, h, cfg, vctx);  // finite throughout: no throw
+    CHECK(val.report.converged);
+    CHECK(std::abs(val.report.iterations - fast.report.iterations) <= 1);
+    double num = 0.0, den = 0.0;
+    for (std::size_t i = 0; i < val.u.size(); ++i) {
+      const double d = val.u.get(i) - fast.u.get(i);
+      num += d * d;
+      den += fast.u.get(i) * fast.u.get(i);
+    }
+    CHECK(std::sqrt(num / den) <= 1e-9);
+    // a non-finite rhs entry: the first axpy (r = b - A u) reports it by index
+    PVector bad = p.b;
+    bad.set(123, std::numeric_limits<double>::infinity());
+    bool thrown = false;
+    try {
+      ir_solve(p.A, bad, h, cfg, vctx);
+    } catch (const ValidationError& e) {
+      thrown = std::string(e.what()).find("index 123") != std::string::npos;
+    }
+    CHECK(thrown);
+    // without validate the same input diverges (non-finite alpha, ir_solver.cpp:97-101)
+    CHECK_THROWS(ir_solve(p.A, bad, h, cfg, ctx), DivergedError);
+    // a V-cycle on a binary16 input holding an infinity
+    PVector rl = cast_vector(p.b, Precision::FP16, norm2_fp64(p.b, ctx), ctx);
+    rl.set(7, std::numeric_limits<double>::infinity());
+    PVector c(rl.size(), Precision::FP16);
+    CHECK_THROWS(h.v_cycle(rl, c, vctx), ValidationError);
+    std::printf("validate mode: %d its (fused %d)\n", val.report.iterations, fast.report.iterations);
   }
   // errors: diverged / build / spec
   CHECK_THROWS((ProblemSpec{3, 1, 66, 6}.validate()), std::invalid_argument);

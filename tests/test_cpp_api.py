@@ -23,7 +23,9 @@ def build_exe():
                    capture_output=True)
     os.makedirs(os.path.dirname(EXE), exist_ok=True)
     src = os.path.join(ROOT, "tests", "cpp", "test_api.cpp")
-    if not os.path.exists(EXE) or os.path.getmtime(EXE) < os.path.getmtime(src):
+    deps = [src, os.path.join(LIB, "libmpmg_cpp.so"), os.path.join(LIB, "libmpmg_b200.so")]
+    deps += [os.path.join(ROOT, "include", "mpmg", f) for f in os.listdir(os.path.join(ROOT, "include", "mpmg"))]
+    if not os.path.exists(EXE) or os.path.getmtime(EXE) < max(os.path.getmtime(d) for d in deps if os.path.exists(d)):
         subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"), src, "-L" + LIB, "-lmpmg_cpp",
                         "-lmpmg_b200", "-Wl,-rpath," + LIB, "-o", EXE], check=True)
     return EXE
