@@ -8,6 +8,7 @@
 
 #include "mpmg_internal.h"
 #include "mpmg_plane.cuh"
+#include "mpmg_row2d.cuh"
 
 namespace mpmg_impl {
 
@@ -167,6 +168,44 @@ struct PlaneLaunch {
   }
 };
 
+// 2D levels through k_row2d: 16 bytes per lane, a 6-stage ring per warp,
+// 4 warps per CTA, persistent grid of >= 8-row runs per warp
+template <int LP, int OP, bool FTZ>
+struct Row2dLaunch {
+  static constexpr int W = 16 / Bytes<LP>::v;
+  static constexpr int NS = 6, WPB = 4;
+  using K = R2<LP, OP, W, NS>;
+  static constexpr int kSmem = WPB * K::WARP_SMEM;
+  static constexpr auto kernel = k_row2d<LP, OP, FTZ, W, NS, WPB>;
+  static int blocks() {
+    static int nb = -1;
+    if (nb < 0) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, 32 * WPB, kSmem);
+      nb = (n > 0 ? n : 1) * plane_num_sms();
+    }
+    return nb;
+  }
+  static cudaError_t run(const PlaneArgs& a, cudaStream_t s) {
+    const long long T = (long long)(a.P / K::SEG) * (a.P - 1);
+    long long nb = blocks();
+    const long long want = (T / 8 + WPB - 1) / WPB;
+    if (want < nb) nb = want > 0 ? want : 1;
+    return launch_pdl(kernel, dim3((unsigned)nb), dim3(32 * WPB), kSmem, s, a);
+  }
+};
+
+// smallest 2D pitch k_row2d takes (MPMG_ROW2D_MINP; 0 disables it)
+inline int row2d_min_pitch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_ROW2D_MINP");
+    v = e ? std::atoi(e) : 64;
+  }
+  return v;
+}
+
 // dispatch on the pitch; returns false when the plane kernels do not cover P
 template <typename F>
 inline bool with_pitch(int P, F&& f) {
@@ -197,6 +236,27 @@ template <int LP>
 bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                     uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr,
                     const int* out_slot = nullptr, long long out_stride = 0) {
+  if (A.dim == 2 && (op == 1 || op == 2 || op == 3) && !slab && !out_slot && (policy & MPMG_FMA) &&
+      !(LP == P16 && (policy & MPMG_ACC32))) {
+    const int P = pitch(A.nodes);
+    constexpr int SEG = 32 * 16 / Bytes<LP>::v;
+    if (row2d_min_pitch() > 0 && P >= row2d_min_pitch() && P >= SEG && P % SEG == 0 && aligned16(x) &&
+        aligned16(b) && aligned16(out)) {
+      PlaneArgs a = plane_args(A, nullptr);
+      a.x = x; a.b = b; a.out = out;
+      const bool ftz = policy & MPMG_FTZ;
+      const double w = round_to(omega, LP, ftz);
+      a.w16 = h2_of(w); a.w32 = (float)w; a.w64 = w;
+      auto go = [&](auto opc) {
+        constexpr int O = decltype(opc)::value;
+        *err = ftz ? Row2dLaunch<LP, O, true>::run(a, s) : Row2dLaunch<LP, O, false>::run(a, s);
+      };
+      if (op == 1) go(std::integral_constant<int, POP_DEFECT>{});
+      else if (op == 3) go(std::integral_constant<int, POP_JACOBI_Z>{});
+      else go(std::integral_constant<int, POP_JACOBI>{});
+      return true;
+    }
+  }
   if (A.dim != 3 || (op != 1 && op != 2 && op != 3)) return false;
   if (pitch(A.nodes) < plane_min_pitch()) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
