@@ -38,13 +38,17 @@ STRIDE = 997  # prime: the sample walks through every x/y/z residue class
 
 def main(variants):
     R = Reference()
-    for spec in variants:  # "h_mg" (FTZ off) or "h_mg:1" (FTZ on, the reference default)
+    for spec in variants:  # "h_mg" (FTZ off), "h_mg:1" (FTZ on, the reference default), "2d:h_mg" (8193^2)
+        dim, n, L = 3, 257, 8
+        if spec.startswith("2d:"):
+            dim, n, L, spec = 2, 8193, 13, spec[3:]
         variant, _, f = spec.partition(":")
         ftz = int(f or 0)
-        path = os.path.join(HERE, f"solves257_{variant}" + ("_ftz1" if ftz else "") + ".npz")
+        tag = "257" if dim == 3 else "8193_2d"
+        path = os.path.join(HERE, f"solves{tag}_{variant}" + ("_ftz1" if ftz else "") + ".npz")
         out = {"stride": np.array(STRIDE)}
         t0 = time.perf_counter()
-        h = R.hierarchy(3, 257, 8, variant, pre=3, post=3, ftz=ftz)
+        h = R.hierarchy(dim, n, L, variant, pre=3, post=3, ftz=ftz)
         build_s = time.perf_counter() - t0
         s = h.ir_solve(rel_tol=1e-10, want_u=True)
         u = s["u"]

@@ -268,6 +268,7 @@ def test_ir_solve_257(variant, ftz):
     g = golden(variant, ftz)
     key = f"{variant}_ftz{int(ftz)}"
     its_ref = int(g[f"{key}_meta"][0])
+    conv_ref = bool(g[f"{key}_meta"][1])
     hist_ref = g[f"{key}_history"]
     stride = int(g["stride"])
     b = mg.problem_rhs(DIM, N)
@@ -275,17 +276,28 @@ def test_ir_solve_257(variant, ftz):
     h = mg.Hierarchy(DIM, N, L, variant, ftz=ftz)
     u, rep = h.ir_solve(b, mg.IrConfig(outer_tolerance=tol))
     h.close()
-    assert rep.converged and bool(g[f"{key}_meta"][1])
-    assert abs(rep.iterations - its_ref) <= 1, (rep.iterations, its_ref)
-    assert rep.final_residual < tol
     # the first residual is ||b|| (u0 = 0) up to the reduction order
     assert rep.residual_history[0] == pytest.approx(hist_ref[0], rel=1e-13)
-    # the trajectory: the same contraction per iteration (a few digits while
-    # far above the rounding level)
-    k = min(len(hist_ref), len(rep.residual_history), 4)
-    np.testing.assert_allclose(rep.residual_history[:k], hist_ref[:k], rtol=1e-3)
     us, ur = u[::stride], g[f"{key}_u_sample"]
     rel = np.linalg.norm(us - ur) / np.linalg.norm(ur)
-    assert rel <= 1e-9, rel
     un = float(np.sqrt(np.dot(u, u)))
-    assert un == pytest.approx(float(g[f"{key}_u_norm"]), rel=1e-9)
+    if conv_ref:
+        assert rep.converged
+        assert abs(rep.iterations - its_ref) <= 1, (rep.iterations, its_ref)
+        assert rep.final_residual < tol
+        # the trajectory: the same contraction per iteration (a few digits while
+        # far above the rounding level)
+        k = min(len(hist_ref), len(rep.residual_history), 4)
+        np.testing.assert_allclose(rep.residual_history[:k], hist_ref[:k], rtol=1e-3)
+        assert rel <= 1e-9, rel
+        assert un == pytest.approx(float(g[f"{key}_u_norm"]), rel=1e-9)
+    else:
+        # the reference default (flush binary16 subnormals after rounding)
+        # stagnates at 257^3: ||r|| contracts ~0.99 per iteration and the solve
+        # stops at max_outer_iterations (100) unconverged -- reproduced here,
+        # trajectory and iterate included
+        assert not rep.converged and rep.iterations == its_ref == 100
+        np.testing.assert_allclose(rep.residual_history, hist_ref, rtol=1e-4)
+        assert rep.final_residual == pytest.approx(float(g[f"{key}_final"]), rel=1e-4)
+        assert rel <= 1e-6, rel
+        assert un == pytest.approx(float(g[f"{key}_u_norm"]), rel=1e-6)
