@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--only-kernels", action="store_true", help="per-kernel timing only (for ncu captures)")
     ap.add_argument("--no-graph", action="store_true",
                     help="host-driven IR loop instead of the graph WHILE node (ncu cannot profile conditional graphs)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the secondary BASELINE configs (HSD_MG 257^3, FTZ-on 257^3, 2D 8193^2)")
     return ap.parse_args()
 
 
@@ -236,6 +238,9 @@ def run_b200(a):
 
     kernels = {} if a.no_kernels else kernel_roofline(a, dim, n, L, ftz, dev, flush_l2)
     clocks = sampler.stop()
+    extra = None
+    if not a.no_extra and ws == 1 and dim == 3 and n == 257 and a.variant == "h_mg" and not ftz:
+        extra = extra_configs(a, dev, flush_l2)
 
     if rank != 0:
         if ws > 1:
@@ -282,6 +287,8 @@ def run_b200(a):
                            "algorithmic_bytes": dom["bytes"], "avg_us": dom["avg_us"],
                            "peak_source": peaks["source"]}
         out["kernels"] = {k: v for k, v in kernels.items() if k != "dominant"}
+    if extra:
+        out["configs"] = extra
     out["clocks"] = clocks
     if not a.no_cpu and ws == 1:
         try:
@@ -291,6 +298,91 @@ def run_b200(a):
     print(json.dumps(out), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def extra_configs(a, dev, flush_l2):
+    """The other BASELINE.json configs on one B200 (device time per solve,
+    L2 flushed before each, CUDA events on the solver stream):
+      configs[2]  3D 257^3 HSD_MG (FP16 fine / FP32 / FP64 coarse) vs D_MG;
+      the reference-default policy (FTZ on) at 257^3: H_MG and D_MG;
+      configs[3]  2D 8193^2 (L = 13) H_MG vs D_MG, plus the finest 2D
+                  Jacobi kernel (k_row2d) against the HBM roofline."""
+    import numpy as np
+    import torch
+
+    import paper_2007_07539_b200 as mg
+    lib = mg.lib()
+    steps = max(2, min(a.steps, 5))
+
+    def solve(dim, n, variant, ftz):
+        L = max_depth(n)
+        b = mg.problem_rhs(dim, n)
+        tol = a.rel_tol * float(np.sqrt(np.dot(b, b)))
+        h = mg.Hierarchy(dim, n, L, variant, ftz=ftz)
+        bd, ud = h.device_buffers()
+        bt = torch.from_numpy(b).to(dev)
+        mg._check(lib.mpmg_gpu_pack(dim, n, mg.FP64, bt.data_ptr(), bd, None), "pack")
+        torch.cuda.synchronize()
+        cfg = mg.IrConfig(outer_tolerance=tol)
+        for _ in range(2):
+            flush_l2()
+            rep = h.ir_solve_ptr(bd, ud, cfg, device=True)
+        times = []
+        for _ in range(steps):
+            flush_l2()
+            rep = h.ir_solve_ptr(bd, ud, cfg, device=True)
+            times.append(rep.device_seconds)
+        h.close()
+        del bt
+        torch.cuda.empty_cache()
+        return {"seconds": float(np.mean(times)), "iterations": rep.iterations, "converged": rep.converged,
+                "final_residual": rep.final_residual, "tolerance": tol, "steps": steps}
+
+    out = {}
+    d0 = solve(3, 257, "d_mg", False)
+    hsd = solve(3, 257, "hsd_mg", False)
+    out["hsd_mg_257"] = {"config": "BASELINE configs[2]: 3D 257^3, L=8, HSD_MG (binary16 levels 3-7, binary32 "
+                                   "level 2, binary64 levels 0-1), FTZ off", **hsd,
+                         "d_mg_seconds": d0["seconds"], "d_mg_iterations": d0["iterations"],
+                         "speedup_vs_fp64": d0["seconds"] / hsd["seconds"]}
+    hf = solve(3, 257, "h_mg", True)
+    df = solve(3, 257, "d_mg", True)
+    out["ftz_on_257"] = {"config": "3D 257^3, L=8, the reference's default policy (binary16 subnormals flushed "
+                                   "after rounding); H_MG stagnates like the reference (100 its, unconverged)",
+                         "h_mg": hf, "d_mg": df}
+    h2 = solve(2, 8193, "h_mg", False)
+    d2 = solve(2, 8193, "d_mg", False)
+    n2 = 8193
+    N2 = mg.unknowns(2, n2)
+    # finest 2D binary16 Jacobi: 3 x 2 bytes x N, operands rotated over 3 sets (> L2)
+    plen = lib.mpmg_padded_len(2, n2)
+    A = mg.level_stencil(2, n2, mg.FP16, False)
+    sets = [(torch.zeros(plen, dtype=torch.float16, device=dev), torch.zeros(plen, dtype=torch.float16, device=dev),
+             torch.zeros(plen, dtype=torch.float16, device=dev)) for _ in range(3)]
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    pol = mg.policy_word(False, True, False)
+    for bb, uu, oo in sets:
+        mg._check(lib.mpmg_gpu_jacobi(C.byref(A), bb.data_ptr(), uu.data_ptr(), oo.data_ptr(), 2.0 / 3.0, pol, sp), "j")
+    flush_l2()
+    reps = 21
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(reps):
+        bb, uu, oo = sets[k % 3]
+        lib.mpmg_gpu_jacobi(C.byref(A), bb.data_ptr(), uu.data_ptr(), oo.data_ptr(), 2.0 / 3.0, pol, sp)
+    e1.record(stream)
+    e1.synchronize()
+    avg = e0.elapsed_time(e1) * 1e-3 / reps
+    peaks = load_peaks()
+    jb = 3 * 2 * N2
+    out["2d_8193"] = {"config": "BASELINE configs[3]: 2D 8193^2 (67,092,481 unknowns), L=13, V(3,3), FTZ off",
+                      "h_mg": h2, "d_mg": d2, "speedup_vs_fp64": d2["seconds"] / h2["seconds"],
+                      "jacobi_fine": {"bytes": jb, "avg_us": avg * 1e6, "achieved_gbs": jb / avg / 1e9,
+                                      "frac": jb / avg / 1e9 / peaks["hbm_gbs"], "kernel": "k_row2d (binary16, 9-pt)"}}
+    del sets
+    torch.cuda.empty_cache()
+    return out
 
 
 def solve_launches(h, iterations, a, variant):
@@ -388,8 +480,8 @@ def kernel_roofline(a, dim, n, L, ftz, dev, flush_l2):
                                                                 s["u64"].data_ptr(), s["r64"].data_ptr(),
                                                                 part.data_ptr(), sp)),
     }
-    if prec == mg.FP64:  # the FP64 finest level keeps the fused update
-        specs.pop("update_r")
+    if prec == mg.FP64 or lib.mpmg_gpu_update_r_partials(dim, n, prec) <= 0:
+        specs.pop("update_r")  # FP64 finest levels (and 2D) keep the fused update
     res = {}
     reps = max(a.kernel_reps, nsets)
     for name, (nbytes, fn) in specs.items():
