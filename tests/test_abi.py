@@ -92,6 +92,16 @@ def test_problem_rhs_bitwise(dim, n):  # assemble_rhs, mesh_fem.cpp:157-202
     assert same_bits(mg.problem_rhs(dim, n), O.rhs(dim, n))
 
 
+@pytest.mark.parametrize("threads", ["1", "3", "16"])
+@pytest.mark.parametrize("dim,n", [(3, 129), (2, 1025), (3, 41)])
+def test_problem_rhs_threaded_bitwise(dim, n, threads, monkeypatch):
+    """The layer-split threaded assembly adds every node's terms in the
+    sequential element order: bitwise the reference's sum for any thread
+    count (mesh_fem.cpp:157-202)."""
+    monkeypatch.setenv("MPMG_RHS_THREADS", threads)
+    assert same_bits(mg.problem_rhs(dim, n), O.rhs(dim, n))
+
+
 def test_padded_layout_sizes():
     L = mg.lib()
     assert L.mpmg_padded_len(3, 257) == 256 ** 3 + 256 ** 2 + 256 + 1
