@@ -23,17 +23,20 @@ int rc(cudaError_t e) { return e == cudaSuccess ? MPMG_OK : set_cuda_error(e); }
 extern "C" {
 
 int mpmg_gpu_pack(int32_t dim, int32_t nodes, int32_t prec, const void* compact, void* padded, void* stream) {
+  clear_stale_error();
   if ((dim != 2 && dim != 3) || nodes < 3 || !valid_prec(prec) || !compact || !padded) return MPMG_EINVAL;
   return rc(launch_pack(dim, nodes, prec, compact, padded, false, (cudaStream_t)stream));
 }
 
 int mpmg_gpu_unpack(int32_t dim, int32_t nodes, int32_t prec, const void* padded, void* compact, void* stream) {
+  clear_stale_error();
   if ((dim != 2 && dim != 3) || nodes < 3 || !valid_prec(prec) || !compact || !padded) return MPMG_EINVAL;
   return rc(launch_pack(dim, nodes, prec, compact, const_cast<void*>(padded), true, (cudaStream_t)stream));
 }
 
 int mpmg_gpu_jacobi(const mpmg_stencil* A, const void* b, const void* u_in, void* u_out, double omega,
                     uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A) || !b || !u_out || u_in == u_out) return MPMG_EINVAL;
   if (!(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;  // multigrid.cpp:82
   if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
@@ -45,12 +48,14 @@ int mpmg_gpu_jacobi(const mpmg_stencil* A, const void* b, const void* u_in, void
 }
 
 int mpmg_gpu_defect(const mpmg_stencil* A, const void* b, const void* u, void* r, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A) || !b || !u || !r || u == r) return MPMG_EINVAL;
   if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
   return rc(launch_level_op(1, *A, u, b, r, 1.0, policy, (cudaStream_t)stream));
 }
 
 int mpmg_gpu_spmv(const mpmg_stencil* A, const void* x, void* y, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A) || !x || !y || x == y) return MPMG_EINVAL;  // kernels.cpp:248 aliasing
   if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
   return rc(launch_level_op(0, *A, x, nullptr, y, 1.0, policy, (cudaStream_t)stream));
@@ -58,6 +63,7 @@ int mpmg_gpu_spmv(const mpmg_stencil* A, const void* x, void* y, uint32_t policy
 
 int mpmg_gpu_restrict(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_t coarse_prec, const void* r_fine,
                       void* r_coarse, const double* scale_dev, uint32_t policy, void* stream) {
+  clear_stale_error();
   if ((dim != 2 && dim != 3) || fine_nodes < 5 || (fine_nodes - 1) % 2 || !valid_prec(fine_prec) ||
       !valid_prec(coarse_prec) || !r_fine || !r_coarse)
     return MPMG_EINVAL;
@@ -68,6 +74,7 @@ int mpmg_gpu_restrict(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_
 int mpmg_gpu_prolong_correct(int32_t dim, int32_t fine_nodes, int32_t fine_prec, int32_t coarse_prec,
                              const void* c_coarse, void* u_fine, const double* scale_dev, uint32_t policy,
                              void* stream) {
+  clear_stale_error();
   if ((dim != 2 && dim != 3) || fine_nodes < 5 || (fine_nodes - 1) % 2 || !valid_prec(fine_prec) ||
       !valid_prec(coarse_prec) || !c_coarse || !u_fine)
     return MPMG_EINVAL;
@@ -77,6 +84,7 @@ int mpmg_gpu_prolong_correct(int32_t dim, int32_t fine_nodes, int32_t fine_prec,
 
 int mpmg_gpu_defect_f64(const mpmg_stencil* A64, const double* b, const double* u, double* r, double* partials,
                         void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A64) || A64->prec != MPMG_FP64 || !b || !u || !r) return MPMG_EINVAL;
   if (!stencil_supported(A64->dim, A64->nodes, MPMG_FP64)) return MPMG_EUNSUPPORTED;
   return rc(launch_defect64(*A64, b, u, r, partials, true, false, (cudaStream_t)stream));
@@ -84,6 +92,7 @@ int mpmg_gpu_defect_f64(const mpmg_stencil* A64, const double* b, const double* 
 
 int mpmg_gpu_update_rc(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, double* u,
                        const double* alpha_dev, double* partials, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A64) || A64->prec != MPMG_FP64 || !c || !valid_prec(c_prec) || !r || !u || !alpha_dev)
     return MPMG_EINVAL;
   if (!stencil_supported(A64->dim, A64->nodes, c_prec)) return MPMG_EUNSUPPORTED;
@@ -93,6 +102,7 @@ int mpmg_gpu_update_rc(const mpmg_stencil* A64, const void* c, int32_t c_prec, d
 int mpmg_gpu_update_r(const mpmg_stencil* A64, const void* c, int32_t c_prec, double* r, const double* alpha_dev,
                       double* partials, void* ring, int64_t ring_len, const int32_t* slot_dev, double* ring_scale,
                       uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A64) || A64->prec != MPMG_FP64 || !c || !valid_prec(c_prec) || !r || !alpha_dev || !ring ||
       ring_len < (int64_t)mpmg_padded_len(A64->dim, A64->nodes) || !slot_dev || !ring_scale)
     return MPMG_EINVAL;
@@ -105,6 +115,7 @@ int mpmg_gpu_update_r(const mpmg_stencil* A64, const void* c, int32_t c_prec, do
 
 int mpmg_gpu_jacobi_slot(const mpmg_stencil* A, const void* b, const void* u_in, void* ring, int64_t ring_len,
                          const int32_t* slot_dev, double omega, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_stencil(A) || !b || !u_in || !ring || !slot_dev) return MPMG_EINVAL;
   if (!(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;  // multigrid.cpp:82
   if (ring_len < (int64_t)mpmg_padded_len(A->dim, A->nodes)) return MPMG_EINVAL;
@@ -119,12 +130,14 @@ int mpmg_gpu_jacobi_slot(const mpmg_stencil* A, const void* b, const void* u_in,
 }
 
 int mpmg_gpu_update_r_partials(int32_t dim, int32_t nodes, int32_t c_prec) {
+  clear_stale_error();
   const int n = plane_update_r_partials(dim, nodes, c_prec);
   return n > 0 ? n : MPMG_EUNSUPPORTED;
 }
 
 int mpmg_gpu_fold(int64_t len, double* u, const void* ring, int64_t ring_len, int32_t c_prec,
                   const double* ring_scale, const int32_t* count_dev, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (len < 1 || !u || !ring || ring_len < len || !valid_prec(c_prec) || !ring_scale || !count_dev) return MPMG_EINVAL;
   return rc(launch_fold((size_t)len, u, ring, (long long)ring_len, c_prec, ring_scale, count_dev, 0, nullptr,
                         policy & MPMG_FMA, (cudaStream_t)stream));
@@ -132,11 +145,13 @@ int mpmg_gpu_fold(int64_t len, double* u, const void* ring, int64_t ring_len, in
 
 int mpmg_gpu_scale_downcast(int32_t dim, int32_t nodes, const double* x, void* out, int32_t prec,
                             const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream) {
+  clear_stale_error();
   if ((dim != 2 && dim != 3) || nodes < 3 || !x || !out || !valid_prec(prec) || !alpha_dev) return MPMG_EINVAL;
   return rc(launch_downcast(dim, nodes, x, out, prec, alpha_dev, scale_enabled, policy, (cudaStream_t)stream));
 }
 
 int mpmg_gpu_partials_len(int32_t dim, int32_t nodes) {
+  clear_stale_error();
   int m = norm2_partials(mpmg_padded_len(dim, nodes));
   for (int lp : {MPMG_FP16, MPMG_FP32, MPMG_FP64})
     for (bool up : {false, true}) {
@@ -148,11 +163,13 @@ int mpmg_gpu_partials_len(int32_t dim, int32_t nodes) {
 
 int mpmg_gpu_norm2_f64(int32_t dim, int32_t nodes, const double* x, double* partials, double* out_dev,
                        void* stream) {
+  clear_stale_error();
   if ((dim != 2 && dim != 3) || nodes < 3 || !x || !partials || !out_dev) return MPMG_EINVAL;
   return rc(launch_norm2(mpmg_padded_len(dim, nodes), x, partials, out_dev, (cudaStream_t)stream));
 }
 
 int mpmg_gpu_norm_finalize(const double* partials, int32_t n_partials, double* out_dev, void* stream) {
+  clear_stale_error();
   if (!partials || n_partials < 0 || !out_dev) return MPMG_EINVAL;
   return rc(launch_norm_finalize(partials, n_partials, out_dev, (cudaStream_t)stream));
 }
@@ -166,6 +183,7 @@ int mpmg_build_stencil(int32_t dim, int32_t nodes, int32_t prec, uint32_t policy
 double mpmg_round_fp16(double x, int32_t ftz) { return round_fp16(x, ftz != 0); }
 
 int mpmg_dev_count(void) {
+  clear_stale_error();
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
     cudaGetLastError();
@@ -189,18 +207,21 @@ void mpmg_dev_free(void* p) {
 }
 
 int mpmg_dev_h2d(void* dst, const void* src, size_t bytes) {
+  clear_stale_error();
   if (!bytes) return MPMG_OK;
   if (!dst || !src) return MPMG_EINVAL;
   return rc(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
 }
 
 int mpmg_dev_d2h(void* dst, const void* src, size_t bytes) {
+  clear_stale_error();
   if (!bytes) return MPMG_OK;
   if (!dst || !src) return MPMG_EINVAL;
   return rc(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
 }
 
 int mpmg_dev_memset0(void* p, size_t bytes) {
+  clear_stale_error();
   if (!bytes) return MPMG_OK;
   if (!p) return MPMG_EINVAL;
   return rc(cudaMemset(p, 0, bytes));
@@ -229,6 +250,7 @@ size_t mpmg_slab_len(int32_t nodes, int32_t nz) {
 
 int mpmg_gpu_slab_jacobi(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u_in, void* u_out,
                          double omega, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_slab(A, s) || !b || !u_out || u_in == u_out || !(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;
   const cudaStream_t q = (cudaStream_t)stream;
   const bool ftz = policy & MPMG_FTZ;
@@ -245,6 +267,7 @@ int mpmg_gpu_slab_jacobi(const mpmg_stencil* A, const mpmg_slab* s, const void* 
 
 int mpmg_gpu_slab_defect(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u, void* r,
                          uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_slab(A, s) || !b || !u || !r || u == r) return MPMG_EINVAL;
   const cudaStream_t q = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
@@ -257,6 +280,7 @@ int mpmg_gpu_slab_defect(const mpmg_stencil* A, const mpmg_slab* s, const void* 
 
 int mpmg_gpu_slab_restrict(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_slab* sc, int32_t fine_prec,
                            int32_t coarse_prec, const void* r_fine, void* r_coarse, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!sf || !sc || !r_fine || !r_coarse || !valid_prec(fine_prec) || !valid_prec(coarse_prec) ||
       (fine_nodes - 1) % 2 || 2 * sc->z_lo < sf->z_lo || 2 * (sc->z_lo + sc->nz - 1) + 1 > sf->z_lo + sf->nz)
     return MPMG_EINVAL;
@@ -267,6 +291,7 @@ int mpmg_gpu_slab_restrict(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_s
 int mpmg_gpu_slab_prolong_correct(int32_t fine_nodes, const mpmg_slab* sf, const mpmg_slab* sc, int32_t fine_prec,
                                   int32_t coarse_prec, const void* c_coarse, void* u_fine, uint32_t policy,
                                   void* stream) {
+  clear_stale_error();
   if (!sf || !sc || !c_coarse || !u_fine || !valid_prec(fine_prec) || !valid_prec(coarse_prec) || (fine_nodes - 1) % 8)
     return MPMG_EINVAL;
   return rc(launch_prolong_slab(fine_nodes, *sf, *sc, fine_prec, coarse_prec, c_coarse, u_fine, policy,
@@ -275,6 +300,7 @@ int mpmg_gpu_slab_prolong_correct(int32_t fine_nodes, const mpmg_slab* sf, const
 
 int mpmg_gpu_slab_defect_f64(const mpmg_stencil* A64, const mpmg_slab* s, const double* b, const double* u,
                              double* r, double* partials, int32_t resnorm, void* stream) {
+  clear_stale_error();
   if (!valid_slab(A64, s) || A64->prec != MPMG_FP64 || !b || !u || (!r && !resnorm)) return MPMG_EINVAL;
   cudaError_t e = cudaSuccess;
   return plane_defect64(*A64, b, u, r, partials, true, resnorm != 0, (cudaStream_t)stream, nullptr, &e, s)
@@ -284,6 +310,7 @@ int mpmg_gpu_slab_defect_f64(const mpmg_stencil* A64, const mpmg_slab* s, const 
 
 int mpmg_gpu_slab_update_rc(const mpmg_stencil* A64, const mpmg_slab* s, const void* c, int32_t c_prec, double* r,
                             double* u, const double* alpha_dev, double* partials, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!valid_slab(A64, s) || A64->prec != MPMG_FP64 || !c || !valid_prec(c_prec) || !r || !u || !alpha_dev)
     return MPMG_EINVAL;
   cudaError_t e = cudaSuccess;
@@ -294,17 +321,20 @@ int mpmg_gpu_slab_update_rc(const mpmg_stencil* A64, const mpmg_slab* s, const v
 
 int mpmg_gpu_slab_scale_downcast(int32_t nodes, const mpmg_slab* s, const double* x, void* out, int32_t prec,
                                  const double* alpha_dev, int32_t scale_enabled, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (!s || s->nz < 1 || nodes < 3 || !x || !out || !valid_prec(prec) || !alpha_dev) return MPMG_EINVAL;
   return rc(launch_downcast_len(mpmg_slab_len(nodes, s->nz), x, out, prec, alpha_dev, scale_enabled, policy,
                                 (cudaStream_t)stream));
 }
 
 int mpmg_gpu_slab_partials_len(int32_t nodes, const mpmg_slab* s, int32_t c_prec, int32_t update) {
+  clear_stale_error();
   if (!s || s->nz < 1) return MPMG_EINVAL;
   return plane_partials(3, nodes, c_prec, update != 0, s->nz + 1);
 }
 
 int mpmg_gpu_partials_sum(const double* partials, int32_t n, double* out_dev, void* stream) {
+  clear_stale_error();
   if (!partials || n < 0 || !out_dev) return MPMG_EINVAL;
   return rc(launch_partials_sum(partials, n, out_dev, (cudaStream_t)stream));
 }

@@ -214,6 +214,7 @@ extern "C" {
 
 int mpmg_gpu_ell_spmv(int64_t rows, int32_t rw, const int32_t* col, const void* val, int32_t prec, const void* x,
                       void* y, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (rows < 0 || rw < 1 || !vp(prec) || !col || !val || !x || !y || x == y) return MPMG_EINVAL;
   if (rows == 0) return MPMG_OK;
   const cudaStream_t s = (cudaStream_t)stream;
@@ -232,6 +233,7 @@ int mpmg_gpu_ell_spmv(int64_t rows, int32_t rw, const int32_t* col, const void* 
 
 int mpmg_gpu_axpy(int64_t n, int32_t prec, double alpha, const void* x, const void* y, void* out, uint32_t policy,
                   void* stream) {
+  clear_stale_error();
   if (n < 0 || !vp(prec) || !x || !y || !out) return MPMG_EINVAL;
   if (n == 0) return MPMG_OK;
   return rc(by_prec(prec, [&](auto pc) -> cudaError_t {
@@ -245,6 +247,7 @@ int mpmg_gpu_axpy(int64_t n, int32_t prec, double alpha, const void* x, const vo
 
 int mpmg_gpu_vec_multiply(int64_t n, int32_t prec, const void* a, const void* b, void* out, uint32_t policy,
                           void* stream) {
+  clear_stale_error();
   if (n < 0 || !vp(prec) || !a || !b || !out) return MPMG_EINVAL;
   if (n == 0) return MPMG_OK;
   return rc(by_prec(prec, [&](auto pc) -> cudaError_t {
@@ -259,6 +262,7 @@ int mpmg_gpu_vec_multiply(int64_t n, int32_t prec, const void* a, const void* b,
 int mpmg_gpu_ell_transfer(int64_t rows, int32_t rw, const int32_t* col, const void* val, int32_t mat_prec,
                           const void* x, int32_t x_prec, int32_t out_prec, const double* scale_dev, int32_t divide,
                           void* out, double* prod, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (rows < 0 || rw < 1 || !col || !val || !x || !vp(mat_prec) || !vp(x_prec) || !vp(out_prec) || (!out && !prod))
     return MPMG_EINVAL;
   if (rows == 0) return MPMG_OK;
@@ -279,6 +283,7 @@ int mpmg_gpu_ell_transfer(int64_t rows, int32_t rw, const int32_t* col, const vo
 int mpmg_gpu_ell_update_rc(int64_t rows, int32_t rw, const int32_t* col, const double* val, const void* c,
                            int32_t c_prec, double* r, double* u, const double* alpha_dev, uint32_t policy,
                            void* stream) {
+  clear_stale_error();
   if (rows < 0 || rw < 1 || !col || !val || !c || !vp(c_prec) || !r || !u || !alpha_dev) return MPMG_EINVAL;
   if (rows == 0) return MPMG_OK;
   return rc(by_prec(c_prec, [&](auto cp) -> cudaError_t {
@@ -293,6 +298,7 @@ int mpmg_gpu_ell_update_rc(int64_t rows, int32_t rw, const int32_t* col, const d
 
 int mpmg_gpu_cast(int64_t n, const void* x, int32_t x_prec, void* out, int32_t out_prec, const double* scale_dev,
                   double scale, uint32_t policy, void* stream) {
+  clear_stale_error();
   if (n < 0 || !x || !out || !vp(x_prec) || !vp(out_prec)) return MPMG_EINVAL;
   if (!scale_dev && !(scale > 0.0 && scale < INFINITY)) return MPMG_EINVAL;  // kernels.cpp:345
   if (n == 0) return MPMG_OK;
@@ -309,6 +315,7 @@ int mpmg_gpu_cast(int64_t n, const void* x, int32_t x_prec, void* out, int32_t o
 
 int mpmg_gpu_dot_seq(int64_t n, const void* x, int32_t x_prec, const void* y, int32_t y_prec, double* out_dev,
                      int32_t take_sqrt, void* stream) {
+  clear_stale_error();
   if (n < 0 || !x || !y || !out_dev || !vp(x_prec) || !vp(y_prec)) return MPMG_EINVAL;
   return rc(by_prec(x_prec, [&](auto xp) -> cudaError_t {
     return by_prec(y_prec, [&](auto yp) -> cudaError_t {
@@ -320,6 +327,7 @@ int mpmg_gpu_dot_seq(int64_t n, const void* x, int32_t x_prec, const void* y, in
 }
 
 int mpmg_gpu_find_nonfinite(int64_t n, const void* x, int32_t x_prec, int64_t* index, void* stream) {
+  clear_stale_error();
   if (n < 0 || !x || !vp(x_prec) || !index) return MPMG_EINVAL;
   *index = -1;
   if (n == 0) return MPMG_OK;

@@ -14,6 +14,12 @@ namespace mpmg_impl {
 
 inline int pitch(int nodes) { return nodes - 1; }
 
+// C-ABI entry points start from a clean error state: a non-sticky error
+// left behind by an unrelated runtime call of the host process (it would
+// otherwise surface as this call's launch error through cudaGetLastError).
+// Sticky device faults persist and are still reported.
+inline void clear_stale_error() { (void)cudaGetLastError(); }
+
 // launch with programmatic dependent launch enabled (MPMG_PDL=0 disables);
 // the kernel must call mpmg_dev::pdl_wait() before reading predecessor data
 bool pdl_enabled();

@@ -463,6 +463,7 @@ int mpmg_problem_rhs(int32_t dim, int32_t nodes, int32_t k, double* b_out) {
 }
 
 mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* err_level) {
+  clear_stale_error();
   auto fail = [&](int code, int level) -> mpmg_solver* {
     if (err) *err = code;
     if (err_level) *err_level = level;
@@ -624,6 +625,7 @@ int mpmg_solver_device_buffers(mpmg_solver* s, double** b_dev, double** u_dev) {
 
 int mpmg_solver_solve_device(mpmg_solver* S, const double* b_dev, double* u_dev, const mpmg_solve_params* pp,
                              double* hist, int32_t hist_cap, mpmg_solve_report* rep) {
+  clear_stale_error();
   if (!S || !pp || !(pp->outer_tolerance > 0.0) || pp->max_outer_iterations < 0) return MPMG_EINVAL;
   const mpmg_solve_params p = *pp;
   cudaStream_t q = S->s;
@@ -703,6 +705,7 @@ int mpmg_solver_solve_device(mpmg_solver* S, const double* b_dev, double* u_dev,
 
 int mpmg_solver_solve(mpmg_solver* S, const double* b_host, double* u_host, const mpmg_solve_params* p,
                       double* hist, int32_t hist_cap, mpmg_solve_report* rep) {
+  clear_stale_error();
   if (!S || !b_host) return MPMG_EINVAL;
   const auto t0 = std::chrono::steady_clock::now();
   const size_t n = mpmg_interior_len(S->cfg.dim, S->cfg.nodes);
@@ -768,6 +771,7 @@ cudaError_t download_values(mpmg_solver* S, int dim, int nodes, int prec, const 
 extern "C" {
 
 int mpmg_solver_v_cycle(mpmg_solver* S, const double* b_host, double* c_host) {
+  clear_stale_error();
   if (!S || !b_host || !c_host) return MPMG_EINVAL;
   Level& F = S->lv.back();
   // use the dedicated rlow buffer as the finest rhs
@@ -793,6 +797,7 @@ int mpmg_solver_coarse_debug(mpmg_solver* S, long long* out, int32_t cap) {
 }
 
 int mpmg_solver_v_cycle_device(mpmg_solver* S, const void* b_dev, void* c_dev, void* stream) {
+  clear_stale_error();
   if (!S || !b_dev || !c_dev) return MPMG_EINVAL;
   Level& F = S->lv.back();
   const cudaStream_t q = stream ? (cudaStream_t)stream : S->s;
@@ -819,6 +824,7 @@ int mpmg_solver_v_cycle_device(mpmg_solver* S, const void* b_dev, void* c_dev, v
 //  COARSE_SOLVE out = CG solution of A_0 u = in0 (level must be 0)
 int mpmg_solver_level_op(mpmg_solver* S, int op, int l, const double* in0, const double* in1, double* out,
                          int32_t steps, double scale) {
+  clear_stale_error();
   if (!S || l < 0 || l >= (int)S->lv.size() || !out) return MPMG_EINVAL;
   Level& L = S->lv[l];
   const int dim = L.A.dim, nodes = L.A.nodes, prec = L.A.prec;
