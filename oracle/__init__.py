@@ -102,6 +102,8 @@ class Oracle:
         L.orc_exact.argtypes = [i, i, i, _dp]
         L.orc_ell_free.argtypes = [C.POINTER(_Ell)]
         L.orc_ell_rows.argtypes = [C.POINTER(_Ell), _ip, _dp]
+        L.orc_spmv_rows.argtypes = [C.POINTER(_Ell), _dp, _dp, i64, i64, _Ctx]
+        L.orc_transfer_rows.argtypes = [C.POINTER(_Ell), _dp, i, _dp, i64, i64, _Ctx]
         L.orc_stiffness_implicit.restype = i; L.orc_stiffness_implicit.argtypes = [i, i, C.POINTER(_Ell)]
         L.orc_hier_build_ex.restype = C.c_void_p
         L.orc_hier_build_ex.argtypes = [i, i, i, i, i, i, d, d, i, i, i, i, C.POINTER(C.c_int), i]
@@ -196,6 +198,19 @@ class Oracle:
     def spmv_e(self, e, x, ctx=None):
         y = np.zeros(e.rows)
         self.L.orc_spmv(C.byref(e), np.ascontiguousarray(x, dtype=np.float64), y, ctx or self.ctx())
+        return y
+
+    def spmv_rows(self, e, x, r0, r1, ctx=None):
+        """rows [r0, r1) of A x (sampled checks at sizes where a whole pass is slow)"""
+        y = np.zeros(r1 - r0)
+        self.L.orc_spmv_rows(C.byref(e), np.ascontiguousarray(x, dtype=np.float64), y, r0, r1, ctx or self.ctx())
+        return y
+
+    def transfer_rows(self, e, x, prec, r0, r1, ctx=None):
+        """rows [r0, r1) of the transfer product (restriction / prolongation) in precision prec"""
+        y = np.zeros(r1 - r0)
+        self.L.orc_transfer_rows(C.byref(e), np.ascontiguousarray(x, dtype=np.float64), prec, y, r0, r1,
+                                 ctx or self.ctx())
         return y
 
     def update_rc_e(self, e, r, u, c, alpha, ctx=None):

@@ -272,6 +272,25 @@ void orc_spmv(const orc_ell* A, const double* x, double* y, orc_ctx ctx) {
   }
 }
 
+/* rows [r0, r1) of y = A x only (the sampled-row checks at 1025^3, where a
+ * whole oracle pass is minutes): the same per-row arithmetic as orc_spmv */
+void orc_spmv_rows(const orc_ell* A, const double* x, double* y, int64_t r0, int64_t r1, orc_ctx ctx) {
+  const int rw = A->rw;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = r0; r < r1; ++r) {
+    ELL_ROW(A, r, c, v)
+    if (A->prec == ORC_FP16 && ctx.acc32) {
+      float acc = 0.0f;
+      for (int j = 0; j < rw; ++j) acc = (float)ar_fma(ORC_FP32, (float)v[j], (float)x[c[j]], acc, ctx);
+      y[r - r0] = orc_quantize_fp16((double)acc, ctx.ftz);
+    } else {
+      double acc = 0.0;
+      for (int j = 0; j < rw; ++j) acc = ar_fma(A->prec, v[j], x[c[j]], acc, ctx);
+      y[r - r0] = acc;
+    }
+  }
+}
+
 /* kernels.cpp:195-212: alpha rounded into the precision first */
 void orc_axpy(int prec, double alpha, const double* x, const double* y, double* out, int64_t n, orc_ctx ctx) {
   const double a = orc_round(alpha, prec, ctx.ftz);
@@ -735,6 +754,29 @@ static void transfer_product(const orc_ell* M, const double* x, int prec, double
       for (int j = 0; j < rw; ++j) acc = ctx.fma ? fma(v[j], x[c[j]], acc) : v[j] * x[c[j]] + acc;
       out[r] = acc;
     }
+  }
+}
+
+/* rows [r0, r1) of the transfer product M x (precision prec, per-op
+ * rounding), the restriction / prolongation of multigrid.cpp:155-205 */
+void orc_transfer_rows(const orc_ell* M, const double* x, int prec, double* out, int64_t r0, int64_t r1,
+                       orc_ctx ctx) {
+  const int rw = M->rw;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = r0; r < r1; ++r) {
+    ELL_ROW(M, r, c, v)
+    double acc = 0.0;
+    if (prec == ORC_FP16) {
+      for (int j = 0; j < rw; ++j) acc = orc_fp16_fma(orc_quantize_fp16(v[j], ctx.ftz), x[c[j]], acc, ctx.ftz, ctx.fma);
+    } else if (prec == ORC_FP32) {
+      float a = 0.0f;
+      for (int j = 0; j < rw; ++j)
+        a = orc_ftz_fp32(ctx.fma ? fmaf((float)v[j], (float)x[c[j]], a) : (float)v[j] * (float)x[c[j]] + a, ctx.ftz);
+      acc = (double)a;
+    } else {
+      for (int j = 0; j < rw; ++j) acc = ctx.fma ? fma(v[j], x[c[j]], acc) : v[j] * x[c[j]] + acc;
+    }
+    out[r - r0] = acc;
   }
 }
 

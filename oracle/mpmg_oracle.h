@@ -68,6 +68,9 @@ void orc_ell_rows(const orc_ell* m, int32_t* cols, double* vals); /* all rows, r
 
 /* kernels.cpp */
 void orc_spmv(const orc_ell* A, const double* x, double* y, orc_ctx ctx);
+void orc_spmv_rows(const orc_ell* A, const double* x, double* y, int64_t r0, int64_t r1, orc_ctx ctx);
+void orc_transfer_rows(const orc_ell* M, const double* x, int prec, double* out, int64_t r0, int64_t r1,
+                       orc_ctx ctx);
 void orc_axpy(int prec, double alpha, const double* x, const double* y, double* out, int64_t n, orc_ctx ctx);
 void orc_vec_multiply(int prec, const double* a, const double* b, double* out, int64_t n, orc_ctx ctx);
 void orc_update_rc(double* r, double* u, const orc_ell* A, const double* c, double alpha, orc_ctx ctx);

@@ -28,7 +28,9 @@ struct PlaneCfg {
   static constexpr int NS0 = kWide && W == 8 ? 3 : 4;
   static constexpr int RY = V == 1 ? 2 : (V == 2 ? 2 : (V == 3 ? 4 : (V == 5 ? 1 : RY0)));
   static constexpr int WY = V == 2 ? 8 : (V == 3 ? 2 : (V == 5 ? 8 : WY0));
-  static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : (V == 10 ? 4 : NS0));
+  // (V = 10 at P = 1024: 3 stages, or the FP64 UPDATE stage (r, u rows of
+  // 8 KB + c rows) would need 256 KB of shared memory)
+  static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : (V == 10 ? (P >= 1024 ? 3 : 4) : NS0));
   static constexpr int OPT = V == 4 ? 1 : (V == 11 ? 4 : 0);
 };
 
@@ -119,6 +121,7 @@ struct PlaneLaunch {
   static constexpr bool SKIPF = CP == P16;
   using K = PlaneK<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
   static constexpr auto kernel = k_plane<LP, CP, EP, OP, FTZ, FMA, SKIPF, C::W, C::WX, C::WY, C::RY, C::NS, C::OPT>;
+  static_assert(K::kSmem + 512 <= 227 * 1024, "plane-kernel shared memory exceeds the sm_100a per-CTA limit");
 
   // grid: y-tiles x z-chunks, z-chunks sized so the grid is about one wave.
   // The wave is that of the FTZ-off/FMA-on build for every policy, so the
@@ -292,16 +295,22 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
                             : PlaneLaunch<LP, LP, LP, POP_DEFECT, false, true, PP>::run(a, s);
     else if (op == 3) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, true, true, PP>::run(a, s)
                                  : PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, false, true, PP>::run(a, s);
-    else if (LP == P16 && PP == 256 && !ftz && plane_variant() > 0) {
-      switch (plane_variant()) {
-        case 1: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 1>::run(a, s); break;
-        case 2: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 2>::run(a, s); break;
-        case 3: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 3>::run(a, s); break;
-        case 4: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 4>::run(a, s); break;
-        default: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 5>::run(a, s); break;
+    else {
+      if constexpr (LP == P16 && PP == 256) {  // tuning shapes (MPMG_PLANE_VARIANT)
+        if (!ftz && plane_variant() > 0) {
+          switch (plane_variant()) {
+            case 1: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 1>::run(a, s); break;
+            case 2: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 2>::run(a, s); break;
+            case 3: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 3>::run(a, s); break;
+            case 4: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 4>::run(a, s); break;
+            default: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 5>::run(a, s); break;
+          }
+          return;
+        }
       }
-    } else *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP>::run(a, s)
-                      : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP>::run(a, s);
+      *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP>::run(a, s)
+                 : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP>::run(a, s);
+    }
   });
 }
 

@@ -401,7 +401,7 @@ struct mpmg_solver {
       cudaGraph_t out = nullptr;
       const cudaError_t e4 = cudaStreamEndCapture(s, &out);
       if (e == cudaSuccess) e = e4;
-      g = out;
+      g = e4 == cudaSuccess ? out : nullptr;  // an invalidated capture hands back no graph to destroy
     }
     cudaStreamDestroy(body_s);
     if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
