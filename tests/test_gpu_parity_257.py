@@ -301,3 +301,26 @@ def test_ir_solve_257(variant, ftz):
         assert rep.final_residual == pytest.approx(float(g[f"{key}_final"]), rel=1e-4)
         assert rel <= 1e-6, rel
         assert un == pytest.approx(float(g[f"{key}_u_norm"]), rel=1e-6)
+
+
+def test_ir_solve_8193_2d():
+    """BASELINE configs[3]: 2D 8193^2 (67,092,481 unknowns), L = 13, H_MG,
+    FTZ off -- against the reference's own solve (tests/golden/
+    make_golden_257.py 2d:h_mg; 14 its, the first cycle raises ||r|| 1800x)."""
+    path = os.path.join(GOLDEN, "solves8193_2d_h_mg.npz")
+    if not os.path.exists(path):
+        pytest.skip("solves8193_2d_h_mg.npz not generated")
+    g = np.load(path)
+    key = "h_mg_ftz0"
+    its_ref, hist_ref, stride = int(g[f"{key}_meta"][0]), g[f"{key}_history"], int(g["stride"])
+    b = mg.problem_rhs(2, 8193)
+    tol = 1e-10 * float(np.sqrt(np.dot(b, b)))
+    h = mg.Hierarchy(2, 8193, 13, "h_mg", ftz=False)
+    u, rep = h.ir_solve(b, mg.IrConfig(outer_tolerance=tol))
+    h.close()
+    assert rep.converged and abs(rep.iterations - its_ref) <= 1, (rep.iterations, its_ref)
+    assert rep.residual_history[0] == pytest.approx(hist_ref[0], rel=1e-13)
+    np.testing.assert_allclose(rep.residual_history[:4], hist_ref[:4], rtol=1e-3)
+    us, ur = u[::stride], g[f"{key}_u_sample"]
+    assert np.linalg.norm(us - ur) / np.linalg.norm(ur) <= 1e-9
+    assert float(np.sqrt(np.dot(u, u))) == pytest.approx(float(g[f"{key}_u_norm"]), rel=1e-9)
