@@ -112,6 +112,12 @@ int mpmg_gpu_jacobi(const mpmg_stencil* A, const void* b, const void* u_in, void
                     uint32_t policy, void* stream);
 
 /* Level defect r = b - A u in the level precision (multigrid.cpp:379-380). */
+/* Steps 1 and 2 of jacobi_smooth from u = 0 (multigrid.cpp:376-377), as the
+ * V-cycle's pre-smoother runs them: one fused pass over b where the plane /
+ * row kernels cover the level (u1 = w D^-1 b formed on the fly), else the
+ * pointwise first step into `tmp` and a streaming second step. */
+int mpmg_gpu_jacobi_from_zero2(const mpmg_stencil* A, const void* b, void* tmp, void* u_out, double omega,
+                               uint32_t policy, void* stream);
 int mpmg_gpu_defect(const mpmg_stencil* A, const void* b, const void* u, void* r, uint32_t policy, void* stream);
 
 /* y = A x in the level precision (kernels.cpp:137-193). */

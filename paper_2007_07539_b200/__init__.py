@@ -128,6 +128,8 @@ def lib():
     L.mpmg_gpu_pack.restype = i; L.mpmg_gpu_pack.argtypes = [i32, i32, i32, vp, vp, vp]
     L.mpmg_gpu_unpack.restype = i; L.mpmg_gpu_unpack.argtypes = [i32, i32, i32, vp, vp, vp]
     L.mpmg_gpu_jacobi.restype = i; L.mpmg_gpu_jacobi.argtypes = [sp, vp, vp, vp, d, u32, vp]
+    L.mpmg_gpu_jacobi_from_zero2.restype = i
+    L.mpmg_gpu_jacobi_from_zero2.argtypes = [sp, vp, vp, vp, d, u32, vp]
     L.mpmg_gpu_defect.restype = i; L.mpmg_gpu_defect.argtypes = [sp, vp, vp, vp, u32, vp]
     L.mpmg_gpu_spmv.restype = i; L.mpmg_gpu_spmv.argtypes = [sp, vp, vp, u32, vp]
     L.mpmg_gpu_restrict.restype = i

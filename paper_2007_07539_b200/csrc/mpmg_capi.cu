@@ -47,6 +47,16 @@ int mpmg_gpu_jacobi(const mpmg_stencil* A, const void* b, const void* u_in, void
   return rc(launch_level_op(2, *A, u_in, b, u_out, omega, policy, s));
 }
 
+int mpmg_gpu_jacobi_from_zero2(const mpmg_stencil* A, const void* b, void* tmp, void* u_out, double omega,
+                               uint32_t policy, void* stream) {
+  clear_stale_error();
+  if (!valid_stencil(A) || !b || !tmp || !u_out || tmp == u_out || b == u_out) return MPMG_EINVAL;
+  if (!(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;  // multigrid.cpp:82
+  if (!stencil_supported(A->dim, A->nodes, A->prec)) return MPMG_EUNSUPPORTED;
+  const double wr = round_to(omega, A->prec, policy & MPMG_FTZ);
+  return rc(launch_jacobi_zero2(*A, b, tmp, u_out, omega, wr, policy, (cudaStream_t)stream));
+}
+
 int mpmg_gpu_defect(const mpmg_stencil* A, const void* b, const void* u, void* r, uint32_t policy, void* stream) {
   clear_stale_error();
   if (!valid_stencil(A) || !b || !u || !r || u == r) return MPMG_EINVAL;

@@ -609,11 +609,15 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
       ST prev = shup(rlast<CP, W>(c));
       ST next = shdn(rfirst<CP, W>(c));
       if constexpr (WX > 1) {
-        if (lane == 0) prev = x0 > 0 ? sload_s<LP, CP>(rp + (x0 - 1) * Bytes<LP>::v) : ST(0);
-        if (lane == 31) next = x0 + W < P ? sload_s<LP, CP>(rp + (x0 + W) * Bytes<LP>::v) : ST(0);
-        if constexpr (K::kJZ) {
-          prev = jz_scalar<CP, FTZ, FMA, ST>(jd, jw, prev);
-          next = jz_scalar<CP, FTZ, FMA, ST>(jd, jw, next);
+        // the neighbour warps' edge values, read raw from the staged row (the
+        // shuffled ones above are already transformed for JACOBI_Z)
+        if (lane == 0) {
+          prev = x0 > 0 ? sload_s<LP, CP>(rp + (x0 - 1) * Bytes<LP>::v) : ST(0);
+          if constexpr (K::kJZ) prev = jz_scalar<CP, FTZ, FMA, ST>(jd, jw, prev);
+        }
+        if (lane == 31) {
+          next = x0 + W < P ? sload_s<LP, CP>(rp + (x0 + W) * Bytes<LP>::v) : ST(0);
+          if constexpr (K::kJZ) next = jz_scalar<CP, FTZ, FMA, ST>(jd, jw, next);
         }
       } else {
         if (lane == 0) prev = ST(0);   // x = -1: only feeds the ghost output x = 0

@@ -103,6 +103,12 @@ def test_level_kernels_1025(prec, n, rng):
     jg = unpack(n, out, prec)
     assert Lb.mpmg_gpu_defect(C.byref(A), bd.data_ptr(), ud.data_ptr(), out.data_ptr(), pol, None) == 0
     dg = unpack(n, out, prec)
+    # the pre-smoother's fused steps 1 + 2 from u = 0 (JACOBI_Z)
+    tmp = t.zeros_like(ud)
+    assert Lb.mpmg_gpu_jacobi_from_zero2(C.byref(A), bd.data_ptr(), tmp.data_ptr(), out.data_ptr(), 2.0 / 3.0, pol,
+                                         None) == 0
+    zg = unpack(n, out, prec)
+    del tmp, out
     w = O.round_vec([2.0 / 3.0], prec, False)[0]
     dinv = O.round_vec([A.inv_diag], prec, False)[0]  # the level's D^-1 (already in prec)
     for z in planes(n - 1):
@@ -113,6 +119,13 @@ def test_level_kernels_1025(prec, n, rng):
         dr = O.vec_multiply(prec, np.full(r1 - r0, dinv), r, ctx)
         jo = O.axpy(prec, w, dr, u[r0:r1], ctx)
         assert same(jg[r0:r1], jo), f"jacobi plane {z}: " + mismatch(jg[r0:r1], jo, r0)
+    # step 1 from zero: u1 = w (d b) (pointwise, whole vector), step 2 on the sampled planes
+    u1 = O.axpy(prec, w, O.vec_multiply(prec, np.full(b.size, dinv), b, ctx), np.zeros(b.size), ctx)
+    for z in planes(n - 1):
+        r0, r1 = rows_of(n, z)
+        r = O.axpy(prec, -1.0, O.spmv_rows(Al, u1, r0, r1, ctx), b[r0:r1], ctx)
+        zo = O.axpy(prec, w, O.vec_multiply(prec, np.full(r1 - r0, dinv), r, ctx), u1[r0:r1], ctx)
+        assert same(zg[r0:r1], zo), f"jacobi-from-zero plane {z}: " + mismatch(zg[r0:r1], zo, r0)
 
 
 @pytest.mark.parametrize("prec", [FP64, FP16])
@@ -146,6 +159,21 @@ def test_transfers_1025(prec, rng):
         tp = O.cast(O.transfer_rows(P, c, prec, r0, r1, ctx), prec, 1.0, ctx)
         po = O.axpy(prec, 1.0, tp, u[r0:r1], ctx)
         assert same(pg[r0:r1], po), f"prolong plane {z}: " + mismatch(pg[r0:r1], po, r0)
+
+
+def test_v_cycle_513_d_mg():
+    """One whole D_MG V-cycle at 513^3 (L = 9: two streaming levels above the
+    pitch-256 ones, pitch 512 with two warps per row) bitwise against the
+    oracle -- the composition, not only the kernels."""
+    n, L = 513, 9
+    ctx = O.ctx(False, True, False)
+    h = mg.Hierarchy(DIM, n, L, "d_mg", ftz=False)
+    ho = O.hierarchy(DIM, n, L, "d_mg", ftz=False, implicit=True)
+    b = mg.problem_rhs(DIM, n)
+    cg, co = h.v_cycle(b), ho.v_cycle(b, ctx)
+    h.close()
+    bad = np.count_nonzero(cg != co)
+    assert bad == 0, f"{bad} mismatches, rel {np.linalg.norm(cg - co) / np.linalg.norm(co):.3e}"
 
 
 @pytest.mark.parametrize("cprec", [FP64, FP16])
