@@ -306,7 +306,8 @@ def extra_configs(a, dev, flush_l2):
       configs[2]  3D 257^3 HSD_MG (FP16 fine / FP32 / FP64 coarse) vs D_MG;
       the reference-default policy (FTZ on) at 257^3: H_MG and D_MG;
       configs[3]  2D 8193^2 (L = 13) H_MG vs D_MG, plus the finest 2D
-                  Jacobi kernel (k_row2d) against the HBM roofline."""
+                  Jacobi kernel (k_row2d) against the HBM roofline;
+      configs[4]  its 1025^3 grid on one GPU, H_MG vs D_MG."""
     import numpy as np
     import torch
 
@@ -315,6 +316,7 @@ def extra_configs(a, dev, flush_l2):
     steps = max(2, min(a.steps, 5))
 
     def solve(dim, n, variant, ftz):
+        big = n > 513
         L = max_depth(n)
         b = mg.problem_rhs(dim, n)
         tol = a.rel_tol * float(np.sqrt(np.dot(b, b)))
@@ -324,11 +326,11 @@ def extra_configs(a, dev, flush_l2):
         mg._check(lib.mpmg_gpu_pack(dim, n, mg.FP64, bt.data_ptr(), bd, None), "pack")
         torch.cuda.synchronize()
         cfg = mg.IrConfig(outer_tolerance=tol)
-        for _ in range(2):
+        for _ in range(1 if big else 2):
             flush_l2()
             rep = h.ir_solve_ptr(bd, ud, cfg, device=True)
         times = []
-        for _ in range(steps):
+        for _ in range(2 if big else steps):
             flush_l2()
             rep = h.ir_solve_ptr(bd, ud, cfg, device=True)
             times.append(rep.device_seconds)
@@ -382,6 +384,13 @@ def extra_configs(a, dev, flush_l2):
                                       "frac": jb / avg / 1e9 / peaks["hbm_gbs"], "kernel": "k_row2d (binary16, 9-pt)"}}
     del sets
     torch.cuda.empty_cache()
+    # configs[4]'s grid on ONE B200 (the slab-decomposed multi-GPU run needs a
+    # multi-GPU node): 1025^3, L = 10
+    h4 = solve(3, 1025, "h_mg", False)
+    d4 = solve(3, 1025, "d_mg", False)
+    out["1025_one_gpu"] = {"config": "BASELINE configs[4]'s grid on one B200: 3D 1025^3 (1,070,599,167 unknowns), "
+                                     "L=10, V(3,3), FTZ off (L2 irrelevant at this size)",
+                           "h_mg": h4, "d_mg": d4, "speedup_vs_fp64": d4["seconds"] / h4["seconds"]}
     return out
 
 
