@@ -189,7 +189,7 @@ int mpmg_gpu_norm_finalize(const double* partials, int32_t n_partials, double* o
  * slab's owned planes; halo planes must have been exchanged beforehand. */
 
 /* one Jacobi step on the owned planes; u_in NULL = first step from zero
- * (pointwise, all local planes) */
+ * (pointwise, owned planes only -- the halo planes are left to the exchange) */
 int mpmg_gpu_slab_jacobi(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u_in, void* u_out,
                          double omega, uint32_t policy, void* stream);
 int mpmg_gpu_slab_defect(const mpmg_stencil* A, const mpmg_slab* s, const void* b, const void* u, void* r,
@@ -366,6 +366,42 @@ int mpmg_solver_level_op(mpmg_solver* s, int op, int level, const double* in0, c
                          int32_t steps, double scale);
 enum { MPMG_OP_SPMV = 0, MPMG_OP_JACOBI = 1, MPMG_OP_DEFECT = 2, MPMG_OP_RESTRICT = 3, MPMG_OP_PROLONG = 4,
        MPMG_OP_COARSE_SOLVE = 5 };
+
+/* ---- multi-GPU z-slab solver (one process per GPU) -------------------------
+ * SURVEY §8e; no reference counterpart (the reference is single-threaded,
+ * multigrid.hpp:96-98). The fine levels are split into z-slabs over `world`
+ * ranks (while the pitch splits into >= min_planes planes per rank), the
+ * coarser levels are agglomerated: every rank gathers the restricted rhs of
+ * the agglomeration level over peer memory and runs the coarse V-cycle
+ * itself (replicated, bitwise identical). Halos, the gather and the norm
+ * partials move by peer-memory copies / stores over NVLink (CUDA IPC handles;
+ * raw pointers between ranks of one process) with device-side sequence flags;
+ * a solve is one CUDA graph with a device WHILE loop per rank.
+ *   create : builds rank `rank`'s buffers and writes its exchange blob
+ *            (*blob_len bytes) -- transport it to every rank (any channel);
+ *   connect: all ranks' blobs concatenated in rank order;
+ *   buffers: this rank's FP64 rhs / solution slabs (local planes 0..nz+1 of
+ *            the finest level, P^2 values each; owned planes 1..nz are global
+ *            planes z_lo..z_lo+nz-1); fill b's owned planes before a solve;
+ *   solve  : every rank calls it; same params on all ranks. u0 = 0 only.
+ * Variants D_MG / H_MG / HSD_MG (no DSH rescaling); 3D. */
+typedef struct mpmg_dist mpmg_dist;
+mpmg_dist* mpmg_dist_create(const mpmg_solver_config* cfg, int32_t rank, int32_t world, int32_t min_planes,
+                            void* blob, size_t blob_cap, size_t* blob_len, int* err);
+int mpmg_dist_connect(mpmg_dist* d, const void* blobs, size_t blob_len);
+void mpmg_dist_destroy(mpmg_dist* d);
+int mpmg_dist_info(const mpmg_dist* d, int32_t* agg_level, int32_t* z_lo, int32_t* nz, size_t* slab_len);
+int mpmg_dist_buffers(mpmg_dist* d, double** b_slab, double** u_slab);
+void* mpmg_dist_stream(mpmg_dist* d);
+/* the agglomeration level's replicated rhs / correction (full padded vectors
+ * in that level's precision), after a solve: the last cycle's */
+int mpmg_dist_agg_buffers(mpmg_dist* d, void** b_full, void** c_full, size_t* len);
+/* builds (captures) the solve graph for these params without running it --
+ * allocation and capture may synchronize the device, so ranks sharing one
+ * GPU (tests) prepare before any of them solves */
+int mpmg_dist_prepare(mpmg_dist* d, const mpmg_solve_params* p);
+int mpmg_dist_solve_device(mpmg_dist* d, const mpmg_solve_params* p, double* hist, int32_t hist_cap,
+                           mpmg_solve_report* rep);
 
 #ifdef __cplusplus
 }

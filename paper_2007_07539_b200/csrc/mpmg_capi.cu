@@ -264,9 +264,13 @@ int mpmg_gpu_slab_jacobi(const mpmg_stencil* A, const mpmg_slab* s, const void* 
   if (!valid_slab(A, s) || !b || !u_out || u_in == u_out || !(omega > 0.0 && omega <= 1.0)) return MPMG_EINVAL;
   const cudaStream_t q = (cudaStream_t)stream;
   const bool ftz = policy & MPMG_FTZ;
-  if (!u_in)
-    return rc(launch_jacobi_zero_len(mpmg_slab_len(A->nodes, s->nz), A->prec, b, u_out, round_to(omega, A->prec, ftz),
+  if (!u_in) {  // owned planes only: the halo planes may be receiving a neighbour's copy right now
+    const size_t pl = (size_t)(A->nodes - 1) * (A->nodes - 1);
+    const size_t off = pl * (size_t)mpmg_bytes_per_value(A->prec);
+    return rc(launch_jacobi_zero_len(pl * (size_t)s->nz, A->prec, static_cast<const unsigned char*>(b) + off,
+                                     static_cast<unsigned char*>(u_out) + off, round_to(omega, A->prec, ftz),
                                      A->inv_diag, policy, q));
+  }
   cudaError_t e = cudaSuccess;
   bool done = false;
   if (A->prec == MPMG_FP16) done = plane_level_op_f16(2, *A, u_in, b, u_out, omega, policy, q, &e, s);

@@ -462,3 +462,91 @@ def compact_of_slabs(slabs, plan, torch_mod=None):
         v = a[: (s.nz + 2) * P * P].reshape(s.nz + 2, P, P)
         out[s.z_lo - 1:s.z_lo - 1 + s.nz] = v[1:1 + s.nz, 1:P, 1:P]
     return out.reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# the C++ multi-GPU solver (csrc/mpmg_dist.cu, include/mpmg_gpu.h mpmg_dist_*)
+# ---------------------------------------------------------------------------
+class DistSolver:
+    """One rank of the C++ z-slab solver: peer-memory halos / gather / norms,
+    one CUDA graph per solve (device WHILE loop). `exchange(blob) -> list of
+    all ranks' blobs` moves the connection blobs (torch.distributed
+    all_gather_object across processes; a plain list within one process)."""
+
+    def __init__(self, nodes, levels, variant, rank, world, ftz=False, pre=3, post=3, device=0, min_planes=4):
+        from . import SolverConfig, VARIANTS, lib, policy_word
+        L = lib()
+        vp, i32, sz = C.c_void_p, C.c_int32, C.c_size_t
+        L.mpmg_dist_create.restype = vp
+        L.mpmg_dist_create.argtypes = [C.POINTER(SolverConfig), i32, i32, i32, vp, sz, C.POINTER(sz),
+                                       C.POINTER(C.c_int)]
+        L.mpmg_dist_connect.restype = C.c_int; L.mpmg_dist_connect.argtypes = [vp, vp, sz]
+        L.mpmg_dist_destroy.argtypes = [vp]
+        L.mpmg_dist_info.restype = C.c_int
+        L.mpmg_dist_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), C.POINTER(sz)]
+        L.mpmg_dist_buffers.restype = C.c_int
+        L.mpmg_dist_buffers.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+        L.mpmg_dist_stream.restype = vp; L.mpmg_dist_stream.argtypes = [vp]
+        from . import SolveParams, SolveReportC
+        L.mpmg_dist_prepare.restype = C.c_int
+        L.mpmg_dist_prepare.argtypes = [vp, C.POINTER(SolveParams)]
+        L.mpmg_dist_solve_device.restype = C.c_int
+        L.mpmg_dist_solve_device.argtypes = [vp, C.POINTER(SolveParams), C.POINTER(C.c_double), i32,
+                                             C.POINTER(SolveReportC)]
+        self.L, self.nodes, self.levels, self.rank, self.world = L, nodes, levels, rank, world
+        cfg = SolverConfig()
+        L.mpmg_solver_default_config(C.byref(cfg))
+        cfg.dim, cfg.nodes, cfg.levels = 3, nodes, levels
+        cfg.variant = VARIANTS[variant] if isinstance(variant, str) else variant
+        cfg.pre_steps, cfg.post_steps = pre, post
+        cfg.policy = policy_word(ftz, True, False)
+        cfg.device = device
+        blob = (C.c_ubyte * 256)()
+        n = C.c_size_t(0)
+        err = C.c_int(0)
+        self.h = L.mpmg_dist_create(C.byref(cfg), rank, world, min_planes, blob, 256, C.byref(n), C.byref(err))
+        if not self.h:
+            raise RuntimeError(f"mpmg_dist_create: code {err.value} ({L.mpmg_last_error().decode()})")
+        self.blob = bytes(blob[: n.value])
+        agg, zlo, nz, slen = C.c_int32(), C.c_int32(), C.c_int32(), C.c_size_t()
+        L.mpmg_dist_info(self.h, C.byref(agg), C.byref(zlo), C.byref(nz), C.byref(slen))
+        self.agg, self.z_lo, self.nz, self.slab_len = agg.value, zlo.value, nz.value, slen.value
+
+    def connect(self, blobs):
+        allb = b"".join(blobs)
+        buf = (C.c_ubyte * len(allb)).from_buffer_copy(allb)
+        rc = self.L.mpmg_dist_connect(self.h, buf, len(self.blob))
+        if rc != 0:
+            raise RuntimeError(f"mpmg_dist_connect: code {rc} ({self.L.mpmg_last_error().decode()})")
+
+    def buffers(self):
+        b, u = C.c_void_p(), C.c_void_p()
+        self.L.mpmg_dist_buffers(self.h, C.byref(b), C.byref(u))
+        return b.value, u.value
+
+    def _params(self, tol, max_it, refresh, scaling):
+        from . import IrConfig
+        return IrConfig(outer_tolerance=tol, max_outer_iterations=max_it, residual_refresh_interval=refresh,
+                        scaling=scaling).c()
+
+    def prepare(self, tol, max_it=100, refresh=10, scaling=0):
+        p = self._params(tol, max_it, refresh, scaling)
+        rc = self.L.mpmg_dist_prepare(self.h, C.byref(p))
+        if rc != 0:
+            raise RuntimeError(f"mpmg_dist_prepare: code {rc} ({self.L.mpmg_last_error().decode()})")
+
+    def solve(self, tol, max_it=100, refresh=10, scaling=0):
+        """every rank calls it (same arguments); returns (report, history)"""
+        from . import SolveReportC
+        p = self._params(tol, max_it, refresh, scaling)
+        hist = (C.c_double * (max_it + 2))()
+        rep = SolveReportC()
+        rc = self.L.mpmg_dist_solve_device(self.h, C.byref(p), hist, max_it + 2, C.byref(rep))
+        if rc != 0:
+            raise RuntimeError(f"mpmg_dist_solve_device: code {rc} ({self.L.mpmg_last_error().decode()})")
+        return rep, np.array(hist[: rep.iterations + 1])
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.mpmg_dist_destroy(self.h)
+            self.h = None

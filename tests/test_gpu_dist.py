@@ -1,0 +1,79 @@
+"""The C++ multi-GPU z-slab solver (csrc/mpmg_dist.cu) on ONE GPU: world = 2
+and 4 ranks in one process (one thread and one stream per rank; raw peer
+pointers instead of IPC handles, the same copies, flags and graphs), against
+the single-GPU solver: the same outer iteration count and the same solution
+(per-point arithmetic is rank-count independent; only the norm's summation
+grouping differs, ~1e-16 in alpha)."""
+import ctypes as C
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2007_07539_b200 as mg
+from paper_2007_07539_b200.dist import DistSolver
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(nodes, levels, variant, world, ftz=False, pre=3, post=3):
+    ranks = [DistSolver(nodes, levels, variant, r, world, ftz=ftz, pre=pre, post=post) for r in range(world)]
+    blobs = [r.blob for r in ranks]
+    for r in ranks:
+        r.connect(blobs)
+    b = mg.problem_rhs(3, nodes)
+    tol = 1e-10 * float(np.sqrt(np.dot(b, b)))
+    P = nodes - 1
+    m = P - 1
+    bc = b.reshape(m, m, m)
+    L = mg.lib()
+    L.mpmg_dev_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    L.mpmg_dev_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    for r in ranks:  # this rank's owned planes of b into its FP64 slab (local planes 1..nz)
+        bptr, _ = r.buffers()
+        slab = np.zeros((r.nz + 2, P, P))
+        slab[1:1 + r.nz, 1:P, 1:P] = bc[r.z_lo - 1:r.z_lo - 1 + r.nz]
+        assert L.mpmg_dev_h2d(bptr, slab.ctypes.data, slab.nbytes) == 0
+    for r in ranks:  # graphs captured up front: capture may synchronize the (shared) device
+        r.prepare(tol)
+    out = [None] * world
+
+    def go(i):
+        out[i] = ranks[i].solve(tol)
+
+    th = [threading.Thread(target=go, args=(i,)) for i in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    # gather u (owned planes) in compact order
+    u = np.zeros((m, m, m))
+    for r in ranks:
+        _, uptr = r.buffers()
+        v = np.zeros((r.nz + 2, P, P))
+        assert L.mpmg_dev_d2h(v.ctypes.data, uptr, v.nbytes) == 0
+        u[r.z_lo - 1:r.z_lo - 1 + r.nz] = v[1:1 + r.nz, 1:P, 1:P]
+    for r in ranks:
+        r.close()
+    return out, u.reshape(-1), b, tol
+
+
+@pytest.mark.parametrize("variant", ["h_mg", "d_mg", "hsd_mg"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_matches_single_gpu(variant, world):
+    nodes, levels = 257, 8
+    out, u, b, tol = run_ranks(nodes, levels, variant, world)
+    reps = [o[0] for o in out]
+    hists = [o[1] for o in out]
+    # identical control flow on every rank
+    assert len({r.iterations for r in reps}) == 1 and all(np.array_equal(hists[0], h) for h in hists)
+    h = mg.Hierarchy(3, nodes, levels, variant, ftz=False)
+    u1, rep1 = h.ir_solve(b, mg.IrConfig(outer_tolerance=tol))
+    h.close()
+    assert reps[0].converged and rep1.converged
+    assert reps[0].iterations == rep1.iterations, (reps[0].iterations, rep1.iterations)
+    # the trajectory agrees to the rounding level of each entry (the norm's
+    # summation grouping differs; FP16 scaled casts may round 1 ulp apart)
+    np.testing.assert_allclose(hists[0], rep1.residual_history, rtol=1e-3)
+    assert np.linalg.norm(u - u1) / np.linalg.norm(u1) <= 1e-9
+    assert reps[0].final_residual < tol
