@@ -611,70 +611,97 @@ def run_reference(a):
 
 
 def run_dist(a):
-    """N > 1: the z-slab decomposed solve (paper_2007_07539_b200.dist) of the
-    same workload over NCCL, one rank per GPU; time = max over ranks of the
-    CUDA-event time of one solve (strong scaling: the problem is fixed)."""
+    """N > 1 (torchrun, one process per GPU): BASELINE configs[4], 3D 1025^3
+    (L = 10) -- strong scaling of the C++ z-slab solver (csrc/mpmg_dist.cu:
+    peer-memory halos over NVLink through CUDA IPC, replicated agglomerated
+    coarse cycle, one CUDA graph per solve). torch.distributed (NCCL) only
+    moves the connection blobs and provides the barriers; the time is the max
+    over ranks of each rank's CUDA-event time of one solve."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2007_07539_b200 as mg
-    from paper_2007_07539_b200.dist import Comm, CudaOps, SlabPlan, SlabSolver, slab_of_compact
+    from paper_2007_07539_b200.dist import DistSolver
 
     ws, rank, local = dist_info()
+    # MPMG_DIST_BACKEND=gloo + fewer GPUs than ranks: the ranks share GPUs
+    # (a functional run of the multi-process path on a one-GPU box; NCCL
+    # refuses two ranks per GPU -- the data path does not use it anyway)
+    backend = os.environ.get("MPMG_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dim, n = a.dim, a.nodes
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    tdev = "cuda" if backend == "nccl" else "cpu"
+    dim, n = 3, (a.nodes if a.nodes != 257 else 1025)
     L = a.levels or max_depth(n)
     ftz = bool(a.ftz)
+    t0 = time.perf_counter()
     b = mg.problem_rhs(dim, n)
+    rhs_s = time.perf_counter() - t0
     tol = a.rel_tol * float(np.sqrt(np.dot(b, b)))
-    plan = SlabPlan(n, L, ws)
-    ops = CudaOps(plan, a.variant, ftz, pre=a.pre, post=a.post)
-    comm = Comm(dist, rank, ws, device_tensors=True)
-    S = SlabSolver(plan, ops, comm)
-    bs = slab_of_compact(b, plan, rank, torch, "cuda")
-    stream = torch.cuda.current_stream()
-    times, its, final = [], 0, 0.0
+    d = DistSolver(n, L, a.variant, rank, ws, ftz=ftz, pre=a.pre, post=a.post, device=local)
+    blobs = [None] * ws
+    dist.all_gather_object(blobs, d.blob)
+    d.connect(blobs)
+    P, m = n - 1, n - 2
+    lib = mg.lib()
+    lib.mpmg_dev_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    lib.mpmg_dev_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    slab = np.zeros((d.nz + 2, P, P))
+    slab[1:1 + d.nz, 1:P, 1:P] = b.reshape(m, m, m)[d.z_lo - 1:d.z_lo - 1 + d.nz]
+    del b
+    bptr, uptr = d.buffers()
+    mg._check(lib.mpmg_dev_h2d(bptr, slab.ctypes.data, slab.nbytes), "h2d")
+    d.prepare(tol)
+    sampler = ClockSampler(local)
+    times, rep = [], None
     for k in range(a.warmup + a.steps):
         dist.barrier()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        u, its, hist, conv, final = S.solve(bs, tol)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        if k == a.warmup:
+            sampler.start()
+        rep, hist = d.solve(tol)
         if k >= a.warmup:
-            times.append(e0.elapsed_time(e1) * 1e-3)
-    t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
+            times.append(rep.device_seconds)
+    clocks = sampler.stop()
+    t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device=tdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    # end to end: this rank's host rhs slab in, host solution slab out
+    # end to end: this rank's host rhs slab in (pinned), solve, host solution slab out
+    bh = torch.from_numpy(slab).pin_memory()
+    uh = torch.empty_like(bh).pin_memory()
     dist.barrier()
     t0 = time.perf_counter()
-    bh = slab_of_compact(b, plan, rank, torch, "cpu").pin_memory()
-    bd = bh.to("cuda", non_blocking=True)
-    u, its2, _, _, _ = S.solve(bd, tol)
-    uh = u.cpu()
-    torch.cuda.synchronize()
-    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    mg._check(lib.mpmg_dev_h2d(bptr, bh.data_ptr(), bh.numel() * 8), "h2d")
+    rep2, _ = d.solve(tol)
+    mg._check(lib.mpmg_dev_d2h(uh.data_ptr(), uptr, uh.numel() * 8), "d2h")
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=tdev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     if rank == 0:
         N = mg.unknowns(dim, n)
         out = {"metric": METRIC, "value": float(t.item()), "unit": UNIT, "n_gpus": ws, "steps": a.steps,
                "warmup": a.warmup, "ms_per_step": float(t.item()) * 1e3, "higher_is_better": False,
-               "scaling": "strong", "vs_baseline": None, "dtype": "fp16" if a.variant == "h_mg" else "mixed",
-               "data": "synthetic: the reference's manufactured Poisson problem, u0 = 0",
-               "config": {"workload": f"{dim}D Poisson {n}^{dim} ({N} unknowns), L={L}, V({a.pre},{a.post}), "
-                                      f"{a.variant.upper()} IR to {a.rel_tol:g}*||b||, z-slabs over {ws} GPUs",
+               "scaling": "strong", "vs_baseline": None,
+               "dtype": "fp16" if a.variant == "h_mg" else ("fp64" if a.variant == "d_mg" else "mixed"),
+               "data": "synthetic: the reference's manufactured Poisson problem (assemble_rhs k=1), u0 = 0",
+               "config": {"workload": f"BASELINE configs[4]: {dim}D Poisson {n}^{dim} ({N} unknowns), L={L}, "
+                                      f"V({a.pre},{a.post}), {a.variant.upper()} IR to {a.rel_tol:g}*||b||, "
+                                      f"z-slabs over {ws} GPUs",
                           "variant": a.variant, "policy": {"flush_subnormals_to_zero": ftz, "fused_multiply_add": True},
-                          "parallelism": f"z-slab decomposition x{ws} (NCCL halo exchange), coarse levels <= "
-                                         f"{plan.P[plan.agg]}^3 agglomerated on rank 0",
-                          "l2": "no flush (strong-scaling run)"},
-               "iterations": its, "final_residual": final, "tolerance": tol, "converged": bool(final < tol),
-               "e2e": {"value": float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(bh.numel() * 8 * ws),
-                       "d2h_bytes_per_step": int(uh.numel() * 8 * ws), "path": "dist.SlabSolver (host slabs)"},
+                          "parallelism": f"z-slab decomposition x{ws}: peer-memory halos (CUDA IPC over NVLink), "
+                                         f"levels <= level {d.agg} agglomerated (replicated coarse cycle)",
+                          "l2": "not flushed (the finest FP64 slabs exceed L2 at every N <= 8)"},
+               "iterations": rep.iterations, "converged": bool(rep.converged), "final_residual": rep.final_residual,
+               "tolerance": tol, "rhs_assembly_s": rhs_s, "clocks": clocks,
+               "e2e": {"value": float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(slab.nbytes * ws),
+                       "d2h_bytes_per_step": int(slab.nbytes * ws), "path": "mpmg_dist_solve_device (C ABI), slabs"},
                "gpu_launches": None}
         print(json.dumps(out), flush=True)
+    dist.barrier()
+    d.close()
     dist.destroy_process_group()
 
 

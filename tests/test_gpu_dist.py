@@ -77,3 +77,70 @@ def test_dist_matches_single_gpu(variant, world):
     np.testing.assert_allclose(hists[0], rep1.residual_history, rtol=1e-3)
     assert np.linalg.norm(u - u1) / np.linalg.norm(u1) <= 1e-9
     assert reps[0].final_residual < tol
+
+
+def _proc(rank, world, port, nodes, levels, variant, q):
+    """one rank per PROCESS (the deployment shape): CUDA IPC handles for the
+    peer arenas, gloo (torch.distributed) only to move the connection blobs"""
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        d = DistSolver(nodes, levels, variant, rank, world)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, d.blob)
+        d.connect(blobs)
+        b = mg.problem_rhs(3, nodes)
+        tol = 1e-10 * float(np.sqrt(np.dot(b, b)))
+        P, m = nodes - 1, nodes - 2
+        slab = np.zeros((d.nz + 2, P, P))
+        slab[1:1 + d.nz, 1:P, 1:P] = b.reshape(m, m, m)[d.z_lo - 1:d.z_lo - 1 + d.nz]
+        L = mg.lib()
+        L.mpmg_dev_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+        L.mpmg_dev_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+        bptr, uptr = d.buffers()
+        assert L.mpmg_dev_h2d(bptr, slab.ctypes.data, slab.nbytes) == 0
+        d.prepare(tol)
+        dist.barrier()
+        rep, hist = d.solve(tol)
+        v = np.zeros((d.nz + 2, P, P))
+        assert L.mpmg_dev_d2h(v.ctypes.data, uptr, v.nbytes) == 0
+        q.put((rank, rep.iterations, bool(rep.converged), hist.tolist(), d.z_lo, d.nz, v[1:1 + d.nz, 1:P, 1:P].copy()))
+        dist.barrier()
+        d.close()
+        dist.destroy_process_group()
+    except Exception as ex:  # reported to the parent
+        q.put((rank, "ERROR " + repr(ex)))
+
+
+def test_dist_two_processes_ipc():
+    import multiprocessing as mp
+    import socket
+    nodes, levels, world = 65, 6, 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_proc, args=(r, world, port, nodes, levels, "h_mg", q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    errs = [r for r in res if isinstance(r[1], str)]
+    assert not errs, errs
+    res.sort(key=lambda r: r[0])
+    m = nodes - 2
+    u = np.zeros((m, m, m))
+    for _, its, conv, hist, z_lo, nz, own in res:
+        u[z_lo - 1:z_lo - 1 + nz] = own
+    assert res[0][1] == res[1][1] and res[0][3] == res[1][3]  # identical control flow
+    b = mg.problem_rhs(3, nodes)
+    tol = 1e-10 * float(np.sqrt(np.dot(b, b)))
+    h = mg.Hierarchy(3, nodes, levels, "h_mg", ftz=False)
+    u1, rep1 = h.ir_solve(b, mg.IrConfig(outer_tolerance=tol))
+    h.close()
+    assert res[0][2] and res[0][1] == rep1.iterations
+    assert np.linalg.norm(u.reshape(-1) - u1) / np.linalg.norm(u1) <= 1e-9
