@@ -290,12 +290,12 @@ def run_b200(a):
             # the binary16 27-point step is FMA-pipe bound on sm_100a: HFMA2 issues
             # at 0.5 warp-instructions / clock / SM sub-partition (measured,
             # profiles/round2_probe_hfma2_rate.txt); 21 live taps + the 3-op
-            # epilogue = 12 HFMA2-class instructions per 2 unknowns
+            # epilogue = 12 HFMA2-class thread-instructions per unknown
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             mhz = float(clocks.get("sm_mhz") or 1965.0)
-            floor_us = (12.0 * N / 64.0) * 2.0 / (sms * 4) / (mhz * 1e6) * 1e6
+            floor_us = (12.0 * N / 32.0) * 2.0 / (sms * 4) / (mhz * 1e6) * 1e6  # warp-instructions x 2 clk
             out["roofline"]["fma_pipe"] = {"floor_us": floor_us, "frac": floor_us / dom["avg_us"],
-                                           "model": "12 HFMA2 per 2 unknowns at 0.5 warp-inst/clk/SMSP"}
+                                           "model": "12 HFMA2-class thread-instructions per unknown at 0.5 warp-inst/clk/SMSP"}
         out["kernels"] = {k: v for k, v in kernels.items() if k != "dominant"}
     if extra:
         out["configs"] = extra
