@@ -233,13 +233,22 @@ void MgHierarchy::v_cycle(const PVector& b, PVector& c, const ExecContext& ctx) 
   require(b.size() == levels_.back().unknowns(), "v_cycle: dimension mismatch");
   require(c.size() == levels_.back().unknowns(), "v_cycle: output dimension mismatch");
   if (solvers_ && !ctx.validate) {
-    // the fused stencil V-cycle on the device (values exchanged as binary64);
-    // validate mode runs op for op (every kernel's output checked)
+    // the fused stencil V-cycle on the device: the vectors move in their
+    // storage precision (compact -> padded on the device, no host value
+    // loop); validate mode runs op for op (every kernel's output checked)
     auto* s = static_cast<mpmg_solver*>(device_solver(ctx));
-    std::vector<double> bb(b.size()), cc(c.size());
-    for (std::size_t i = 0; i < b.size(); ++i) bb[i] = b.get(i);
-    check(mpmg_solver_v_cycle(s, bb.data(), cc.data()), "v_cycle");
-    for (std::size_t i = 0; i < c.size(); ++i) c.set(i, cc[i], ctx.policy);  // exact: values are already rounded
+    const int dim = spec_->dim, nodes = spec_->finest_nodes_per_dim, pc = prec_code(b.precision());
+    const std::size_t plen = mpmg_padded_len(dim, nodes), vb = static_cast<std::size_t>(bytes_per_value(b.precision()));
+    DevVec db(b), dc(c.size(), c.precision());
+    DevBuf pb(plen * vb), pcv(plen * vb);
+    check(mpmg_dev_memset0(pb.get(), plen * vb), "v_cycle");
+    check(mpmg_gpu_pack(dim, nodes, pc, db.get(), pb.get(), nullptr), "v_cycle pack");
+    check(mpmg_dev_sync(), "v_cycle");
+    check(mpmg_solver_v_cycle_device(s, pb.get(), pcv.get(), mpmg_solver_stream(s)), "v_cycle");
+    check(mpmg_dev_sync(), "v_cycle");
+    check(mpmg_gpu_unpack(dim, nodes, pc, pcv.get(), dc.get(), nullptr), "v_cycle unpack");
+    check(mpmg_dev_sync(), "v_cycle");
+    dc.to(c);
     add_cycle_traffic(*this, level_traffic_, ctx);
     return;
   }

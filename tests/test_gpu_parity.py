@@ -55,6 +55,7 @@ def oracle_h(dim, n, L, variant, ftz):
 # (variant, dim, nodes, levels, level under test): binary16 and binary64
 # streaming levels of deep hierarchies, binary32 levels of HSD/DSH cascades
 CASES = [(v, 3, 129, 7, l) for v in ("h_mg", "d_mg") for l in (6, 5)] + \
+        [(v, 3, 97, 6, l) for v in ("h_mg", "d_mg") for l in (5, 4)] + \
         [(v, 2, 257, 8, l) for v in ("h_mg", "d_mg") for l in (7, 6)] + \
         [(v, d, n, 3, 2) for v in ("hsd_mg", "dsh_mg") for d, n in ((2, 257), (3, 129))]
 
@@ -98,7 +99,7 @@ def test_level_kernels(variant, dim, n, L, l, ftz, fma, acc32, rng):
 
 
 @pytest.mark.parametrize("variant", ["h_mg", "hsd_mg", "d_mg", "dsh_mg"])
-@pytest.mark.parametrize("dim,n,L", [(3, 65, 6), (2, 257, 8), (3, 33, 5)])
+@pytest.mark.parametrize("dim,n,L", [(3, 65, 6), (2, 257, 8), (3, 33, 5), (3, 97, 6)])
 @pytest.mark.parametrize("ftz", [True, False])
 def test_v_cycle(variant, dim, n, L, ftz, rng):
     h = mg.Hierarchy(dim, n, L, variant, ftz=ftz)
@@ -125,7 +126,7 @@ def test_coarse_solve_matches_cg(rng):
 
 
 @pytest.mark.parametrize("variant", ["h_mg", "hsd_mg", "d_mg", "dsh_mg"])
-@pytest.mark.parametrize("dim,n,L", [(3, 65, 6), (2, 257, 8)])
+@pytest.mark.parametrize("dim,n,L", [(3, 65, 6), (2, 257, 8), (3, 97, 6)])
 @pytest.mark.parametrize("ftz", [True, False])
 @pytest.mark.parametrize("graph", [True, False])
 def test_ir_solve(variant, dim, n, L, ftz, graph):
