@@ -392,6 +392,11 @@ int mpmg_dist_connect(mpmg_dist* d, const void* blobs, size_t blob_len);
 void mpmg_dist_destroy(mpmg_dist* d);
 int mpmg_dist_info(const mpmg_dist* d, int32_t* agg_level, int32_t* z_lo, int32_t* nz, size_t* slab_len);
 int mpmg_dist_buffers(mpmg_dist* d, double** b_slab, double** u_slab);
+/* halo exchanges recorded in the last captured solve graph: those fused into
+ * the producing slab kernel (stores into the neighbours' halo planes) and
+ * those done as kernel + peer copy (MPMG_DIST_FUSE_HALOS=0, or levels the
+ * fused kernel does not cover: pitch <= 64, FP64 u, agglomeration) */
+int mpmg_dist_exchange_stats(const mpmg_dist* d, int32_t* fused, int32_t* copied);
 void* mpmg_dist_stream(mpmg_dist* d);
 /* the agglomeration level's replicated rhs / correction (full padded vectors
  * in that level's precision), after a solve: the last cycle's */

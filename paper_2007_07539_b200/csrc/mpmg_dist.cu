@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -193,6 +194,8 @@ struct mpmg_dist {
   mpmg_solve_params gkey{};
   bool gvalid = false;
   bool connected = false;
+  bool fuse_halos = true;
+  int n_fused = 0, n_copied = 0;  // halo exchanges recorded in the last graph  // MPMG_DIST_FUSE_HALOS=0: kernel + copy exchange
 
   template <typename T = void>
   T* at(size_t off) { return reinterpret_cast<T*>(arena + off); }
@@ -232,6 +235,7 @@ struct mpmg_dist {
   // we send our last plane up and receive from below; fill_hi: every rank's
   // top halo plane (nz + 1) receives its upper neighbour's first owned plane.
   cudaError_t exchange(int l, size_t off, bool fill_lo, bool fill_hi, cudaStream_t q, int bytes = 0) {
+    ++n_copied;
     const DLevel& L = lv[l];
     const size_t pl = (size_t)L.P * L.P * (bytes ? bytes : L.bytes);
     cudaError_t e = cudaSuccess;
@@ -243,7 +247,13 @@ struct mpmg_dist {
       e = cudaMemcpyAsync(peer_at<unsigned char>(rank - 1, off) + (size_t)(t.nz + 1) * pl, at<unsigned char>(off) + pl,
                           pl, cudaMemcpyDeviceToDevice, q);
     }
-    // signal whom we wrote to, wait for whoever writes to us
+    if (e != cudaSuccess) return e;
+    return handshake(fill_lo, fill_hi, q);
+  }
+
+  // signal whom we wrote halos to, wait for whoever writes ours (see exchange)
+  cudaError_t handshake(bool fill_lo, bool fill_hi, cudaStream_t q) {
+    cudaError_t e = cudaSuccess;
     const int* to = fill_lo && fill_hi ? nb_dev : (fill_lo ? hi_dev : lo_dev);
     const int nto = fill_lo && fill_hi ? n_lo_hi : (fill_lo ? n_hi : n_lo);
     const int* from = fill_lo && fill_hi ? nb_dev : (fill_lo ? lo_dev : hi_dev);
@@ -257,6 +267,38 @@ struct mpmg_dist {
       e = cudaGetLastError();
     }
     return e;
+  }
+
+  // a slab JACOBI (op 2) / DEFECT (op 1) of level l writing buffer `out`,
+  // with the halo exchange fused into the kernel: its first / last owned
+  // output planes are also stored straight into the neighbours' halo planes
+  // (peer memory over NVLink), then only the handshake runs. Falls back to
+  // the kernel + copy exchange where the fused kernel does not cover the level.
+  cudaError_t op_push(int op, int l, size_t b, size_t in, size_t out, bool fill_lo, bool fill_hi, cudaStream_t q) {
+    DLevel& L = lv[l];
+    const size_t pl = (size_t)L.P * L.P * L.bytes;
+    void* push_lo = nullptr;  // our first plane -> lower neighbour's top halo (fill_hi)
+    void* push_hi = nullptr;  // our last plane -> upper neighbour's plane 0 (fill_lo)
+    if (fill_hi && rank > 0) push_lo = peer_at<unsigned char>(rank - 1, out) + (size_t)(slab_of(l, rank - 1).nz + 1) * pl;
+    if (fill_lo && rank + 1 < world) push_hi = peer_at<unsigned char>(rank + 1, out);
+    cudaError_t e = cudaSuccess;
+    bool done = false;
+    if (fuse_halos) {
+      if (L.prec == MPMG_FP16)
+        done = plane_level_op_push_f16(op, L.A, at(in), at(b), at(out), cfg.omega, policy(), q, &e, &L.s, push_lo, push_hi);
+      else if (L.prec == MPMG_FP32)
+        done = plane_level_op_push_f32(op, L.A, at(in), at(b), at(out), cfg.omega, policy(), q, &e, &L.s, push_lo, push_hi);
+      else
+        done = plane_level_op_push_f64(op, L.A, at(in), at(b), at(out), cfg.omega, policy(), q, &e, &L.s, push_lo, push_hi);
+    }
+    if (done) {
+      ++n_fused;
+      return e == cudaSuccess ? handshake(fill_lo, fill_hi, q) : e;
+    }
+    const int rc = op == 2 ? mpmg_gpu_slab_jacobi(&L.A, &L.s, at(b), at(in), at(out), cfg.omega, policy(), q)
+                           : mpmg_gpu_slab_defect(&L.A, &L.s, at(b), at(in), at(out), policy(), q);
+    if (rc != MPMG_OK) return cudaErrorUnknown;
+    return exchange(l, out, fill_lo, fill_hi, q);
   }
 
   // the agglomeration level: our owned planes of the restricted rhs into every
@@ -309,15 +351,13 @@ struct mpmg_dist {
       ok(mpmg_gpu_slab_jacobi(&L.A, &L.s, at(L.b), nullptr, at(cur), cfg.omega, policy(), q));
       if (e == cudaSuccess) e = exchange(l, cur, true, true, q);
       for (int k = 1; k < cfg.pre_steps && e == cudaSuccess; ++k) {
-        ok(mpmg_gpu_slab_jacobi(&L.A, &L.s, at(L.b), at(cur), at(other), cfg.omega, policy(), q));
-        if (e == cudaSuccess) e = exchange(l, other, true, true, q);
+        e = op_push(2, l, L.b, cur, other, true, true, q);
         std::swap(cur, other);
       }
     } else {
       e = cudaMemsetAsync(at(cur), 0, L.slab_len * L.bytes, q);
     }
-    if (e == cudaSuccess) ok(mpmg_gpu_slab_defect(&L.A, &L.s, at(L.b), at(cur), at(L.r), policy(), q));
-    if (e == cudaSuccess) e = exchange(l, L.r, true, false, q);  // the restriction reads the lower halo
+    if (e == cudaSuccess) e = op_push(1, l, L.b, cur, L.r, true, false, q);  // the restriction reads the lower halo
     DLevel& C = lv[l - 1];
     if (e == cudaSuccess && C.s.nz > 0)  // (an agglomeration slab may own no plane)
       ok(mpmg_gpu_slab_restrict(L.P + 1, &L.s, &C.s, L.prec, C.prec, at(L.r), at(C.b), policy(), q));
@@ -328,8 +368,7 @@ struct mpmg_dist {
       ok(mpmg_gpu_slab_prolong_correct(L.P + 1, &L.s, &C.s, L.prec, C.prec, at(cc), at(cur), policy(), q));
     if (e == cudaSuccess) e = exchange(l, cur, true, true, q);
     for (int k = 0; k < cfg.post_steps && e == cudaSuccess; ++k) {
-      ok(mpmg_gpu_slab_jacobi(&L.A, &L.s, at(L.b), at(cur), at(other), cfg.omega, policy(), q));
-      if (e == cudaSuccess) e = exchange(l, other, true, true, q);
+      e = op_push(2, l, L.b, cur, other, true, true, q);
       std::swap(cur, other);
     }
     *res = cur;
@@ -424,6 +463,7 @@ struct mpmg_dist {
   cudaError_t build_graph(const mpmg_solve_params& p) {
     if (exec) { cudaGraphExecDestroy(exec); exec = nullptr; }
     gvalid = false;
+    n_fused = n_copied = 0;
     cudaStream_t body_s = nullptr;
     cudaError_t e = cudaStreamCreateWithFlags(&body_s, cudaStreamNonBlocking);
     if (e != cudaSuccess) return e;
@@ -509,6 +549,7 @@ mpmg_dist* mpmg_dist_create(const mpmg_solver_config* cfg, int32_t rank, int32_t
   if (e != cudaSuccess) return fail(set_cuda_error(e));
   auto* D = new mpmg_dist();
   D->cfg = c;
+  if (const char* fe = std::getenv("MPMG_DIST_FUSE_HALOS")) D->fuse_halos = std::atoi(fe) != 0;
   D->rank = rank;
   D->world = world;
   D->levels = c.levels;
@@ -652,6 +693,13 @@ int mpmg_dist_info(const mpmg_dist* D, int32_t* agg_level, int32_t* z_lo, int32_
   if (z_lo) *z_lo = F.s.z_lo;
   if (nz) *nz = F.s.nz;
   if (slab_len) *slab_len = F.slab_len;
+  return MPMG_OK;
+}
+
+int mpmg_dist_exchange_stats(const mpmg_dist* D, int32_t* fused, int32_t* copied) {
+  if (!D) return MPMG_EINVAL;
+  if (fused) *fused = D->n_fused;
+  if (copied) *copied = D->n_copied;
   return MPMG_OK;
 }
 

@@ -71,6 +71,17 @@ int stencil_partials(int dim, int nodes, int lp, bool update);
 // TMA-staged plane kernels (mpmg_plane_*.cu): return false when the shape
 // or policy is not covered (the caller then uses the streaming kernels)
 // (slab: a z-slab of the level, include/mpmg_gpu.h; nullptr = the whole level)
+// z-slab JACOBI (op 2) / DEFECT (op 1) that also stores the boundary output
+// planes into the neighbours' halo planes (multi-GPU, mpmg_dist.cu)
+bool plane_level_op_push_f16(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                             uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab, void* push_lo,
+                             void* push_hi);
+bool plane_level_op_push_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                             uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab, void* push_lo,
+                             void* push_hi);
+bool plane_level_op_push_f64(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                             uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab, void* push_lo,
+                             void* push_hi);
 bool plane_level_op_f16(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                         uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
 bool plane_level_op_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,

@@ -73,6 +73,13 @@ struct PlaneArgs {
   // from ring slot *ring_slot and skips the copy
   const int* out_slot;
   long long out_stride;
+  // OPT bit 3 (z-slab level ops of the multi-GPU solver): the first owned
+  // output plane is also stored into push_lo (the lower neighbour's top halo
+  // plane, over NVLink peer memory) and the last into push_hi (the upper
+  // neighbour's bottom halo plane) -- the halo exchange fused into the
+  // producing kernel
+  void* push_lo;
+  void* push_hi;
 };
 
 // ---- PTX: mbarrier + bulk copy ------------------------------------------
@@ -544,6 +551,15 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
   void* outp = a.out;
   if constexpr ((OPT & 4) != 0)
     outp = static_cast<unsigned char*>(a.out) + (long long)*a.out_slot * a.out_stride * Bytes<EP>::v;
+  // output row store (+ the fused halo push of a slab's boundary planes)
+  auto put = [&](long long gi, int zo, const Row<EP, W>& row) {
+    gstore<EP, W>(outp, gi, row);
+    if constexpr ((OPT & 8) != 0) {
+      const long long in_plane = gi - zo * plane;
+      if (zo == 1 && a.push_lo) gstore<EP, W>(a.push_lo, in_plane, row);
+      if (zo == a.pz - 1 && a.push_hi) gstore<EP, W>(a.push_hi, in_plane, row);
+    }
+  };
   if (tid == 0) {
     for (int k = 0; k < NS - 1 && k < NQ; ++k) issue(k);
   }
@@ -658,7 +674,7 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
       else if constexpr (EP == P16) t = quant16<FTZ, W>(Acc[i]);
       if constexpr (OP == POP_SPMV) {
         if (x0 == 0) rzero_first<EP, W>(t);
-        if (v) gstore<EP, W>(outp, gi, t);
+        if (v) put(gi, zo, t);
       } else if constexpr (OP == POP_DEFECT || OP == POP_JACOBI || OP == POP_JACOBI_Z) {
         Row<EP, W> bb;
         if constexpr (K::kJZ) rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, bb);  // b centre
@@ -669,7 +685,7 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
           Row<EP, W> r = efma<EP, FTZ, FMA, W>(m1, t, bb);  // axpy(-1, t, b)
           if constexpr (OP == POP_DEFECT) {
             if (x0 == 0) rzero_first<EP, W>(r);
-            if (v) gstore<EP, W>(outp, gi, r);
+            if (v) put(gi, zo, r);
           } else {
             const Row<EP, W> dr = emul<EP, FTZ, W>(a.d16, r);  // vec_multiply(inv_diag, r)
             Row<EP, W> uc;
@@ -679,7 +695,7 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
             } else rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
             Row<EP, W> un = efma<EP, FTZ, FMA, W>(a.w16, dr, uc);  // axpy(omega, t, u)
             if (x0 == 0) rzero_first<EP, W>(un);
-            if (v) gstore<EP, W>(outp, gi, un);
+            if (v) put(gi, zo, un);
           }
         } else {
           using ET = typename Sc<EP>::T;
@@ -687,7 +703,7 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
           Row<EP, W> r = efma<EP, FTZ, FMA, W>(m1, t, bb);
           if constexpr (OP == POP_DEFECT) {
             if (x0 == 0) rzero_first<EP, W>(r);
-            if (v) gstore<EP, W>(outp, gi, r);
+            if (v) put(gi, zo, r);
           } else {
             const Row<EP, W> dr = emul<EP, FTZ, W>(dd, r);
             Row<EP, W> uc;
@@ -697,7 +713,7 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
             } else rload<LP, EP, W>(st + (tr + i + 1) * K::kXRow + x0 * Bytes<LP>::v, uc);
             Row<EP, W> un = efma<EP, FTZ, FMA, W>(ww, dr, uc);
             if (x0 == 0) rzero_first<EP, W>(un);
-            if (v) gstore<EP, W>(outp, gi, un);
+            if (v) put(gi, zo, un);
           }
         }
       } else if constexpr (OP == POP_DEFECT64 || OP == POP_RESNORM) {

@@ -11,4 +11,9 @@ bool plane_jacobi_slot_f32(const mpmg_stencil& A, const void* x, const void* b, 
                           const int* slot, double omega, uint32_t policy, cudaStream_t s, cudaError_t* err) {
   return plane_level_op<mpmg_dev::P32>(2, A, x, b, ring, omega, policy, s, err, nullptr, slot, stride);
 }
+bool plane_level_op_push_f32(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                              uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab, void* push_lo,
+                              void* push_hi) {
+  return plane_level_op_push<mpmg_dev::P32>(op, A, x, b, out, omega, policy, s, err, slab, push_lo, push_hi);
+}
 }  // namespace mpmg_impl

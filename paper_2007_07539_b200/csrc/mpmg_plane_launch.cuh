@@ -31,7 +31,7 @@ struct PlaneCfg {
   // (V = 10 at P = 1024: 3 stages, or the FP64 UPDATE stage (r, u rows of
   // 8 KB + c rows) would need 256 KB of shared memory)
   static constexpr int NS = V == 2 ? 3 : (V == 4 ? 3 : (V == 10 ? (P >= 1024 ? 3 : 4) : NS0));
-  static constexpr int OPT = V == 4 ? 1 : (V == 11 ? 4 : 0);
+  static constexpr int OPT = V == 4 ? 1 : (V == 11 ? 4 : (V == 12 ? 8 : 0));
 };
 
 inline int plane_variant() {
@@ -235,6 +235,32 @@ inline bool faces_zero16(const mpmg_stencil& A) {
 
 // level op (1 DEFECT / 2 JACOBI / 3 two JACOBI steps from zero, x = b) through
 // the plane kernels; false if not covered
+// z-slab level op whose boundary output planes are also pushed into the
+// neighbours' halo planes (push_lo / push_hi, either may be null): JACOBI
+// (op 2) and DEFECT (op 1) on 3D slabs; false if not covered
+template <int LP>
+bool plane_level_op_push(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
+                         uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab, void* push_lo,
+                         void* push_hi) {
+  if (A.dim != 3 || !slab || (op != 1 && op != 2)) return false;
+  if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
+  if (LP == P16 && !faces_zero16(A)) return false;
+  if (!aligned16(x) || !aligned16(b) || !aligned16(out) || !aligned16(push_lo) || !aligned16(push_hi)) return false;
+  PlaneArgs a = plane_args(A, slab);
+  a.x = x; a.b = b; a.out = out;
+  a.push_lo = push_lo; a.push_hi = push_hi;
+  const bool ftz = policy & MPMG_FTZ;
+  const double w = round_to(omega, LP, ftz);
+  a.w16 = h2_of(w); a.w32 = (float)w; a.w64 = w;
+  return with_pitch(a.P, [&](auto pc) {
+    constexpr int PP = decltype(pc)::value;
+    if (op == 1) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_DEFECT, true, true, PP, 12>::run(a, s)
+                            : PlaneLaunch<LP, LP, LP, POP_DEFECT, false, true, PP, 12>::run(a, s);
+    else *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI, true, true, PP, 12>::run(a, s)
+                    : PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 12>::run(a, s);
+  });
+}
+
 template <int LP>
 bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b, void* out, double omega,
                     uint32_t policy, cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr,

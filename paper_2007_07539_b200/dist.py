@@ -487,6 +487,8 @@ class DistSolver:
         L.mpmg_dist_buffers.restype = C.c_int
         L.mpmg_dist_buffers.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
         L.mpmg_dist_stream.restype = vp; L.mpmg_dist_stream.argtypes = [vp]
+        L.mpmg_dist_exchange_stats.restype = C.c_int
+        L.mpmg_dist_exchange_stats.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
         from . import SolveParams, SolveReportC
         L.mpmg_dist_prepare.restype = C.c_int
         L.mpmg_dist_prepare.argtypes = [vp, C.POINTER(SolveParams)]
@@ -518,6 +520,13 @@ class DistSolver:
         rc = self.L.mpmg_dist_connect(self.h, buf, len(self.blob))
         if rc != 0:
             raise RuntimeError(f"mpmg_dist_connect: code {rc} ({self.L.mpmg_last_error().decode()})")
+
+    def exchange_stats(self):
+        """(fused, copied): halo exchanges in the last captured solve graph done
+        by the producing kernel's peer stores / by a separate peer copy"""
+        f, c = C.c_int32(), C.c_int32()
+        self.L.mpmg_dist_exchange_stats(self.h, C.byref(f), C.byref(c))
+        return f.value, c.value
 
     def buffers(self):
         b, u = C.c_void_p(), C.c_void_p()

@@ -37,6 +37,7 @@ def run_ranks(nodes, levels, variant, world, ftz=False, pre=3, post=3):
     for r in ranks:  # graphs captured up front: capture may synchronize the (shared) device
         r.prepare(tol)
     out = [None] * world
+    stats = [r.exchange_stats() for r in ranks]
 
     def go(i):
         out[i] = ranks[i].solve(tol)
@@ -55,6 +56,7 @@ def run_ranks(nodes, levels, variant, world, ftz=False, pre=3, post=3):
         u[r.z_lo - 1:r.z_lo - 1 + r.nz] = v[1:1 + r.nz, 1:P, 1:P]
     for r in ranks:
         r.close()
+    run_ranks.stats = stats
     return out, u.reshape(-1), b, tol
 
 
@@ -77,6 +79,24 @@ def test_dist_matches_single_gpu(variant, world):
     np.testing.assert_allclose(hists[0], rep1.residual_history, rtol=1e-3)
     assert np.linalg.norm(u - u1) / np.linalg.norm(u1) <= 1e-9
     assert reps[0].final_residual < tol
+
+
+@pytest.mark.parametrize("variant", ["h_mg", "d_mg"])
+def test_dist_fused_halos_match_copy_exchange(variant, monkeypatch):
+    """the halo planes stored into the neighbours' memory by the producing
+    Jacobi / defect kernel (default) and the kernel + peer-copy exchange
+    (MPMG_DIST_FUSE_HALOS=0) give the identical solve, bit for bit"""
+    nodes, levels, world = 257, 8, 4
+    monkeypatch.setenv("MPMG_DIST_FUSE_HALOS", "0")
+    out0, u0, _, _ = run_ranks(nodes, levels, variant, world)
+    assert all(f == 0 and c > 0 for f, c in run_ranks.stats)
+    monkeypatch.setenv("MPMG_DIST_FUSE_HALOS", "1")
+    out1, u1, _, _ = run_ranks(nodes, levels, variant, world)
+    # the slab Jacobi sweeps and defects of pitch 256 and 128 fused
+    assert all(f > 0 for f, _ in run_ranks.stats), run_ranks.stats
+    assert out0[0][0].iterations == out1[0][0].iterations
+    assert np.array_equal(out0[0][1], out1[0][1])
+    assert np.array_equal(u0, u1)
 
 
 def _proc(rank, world, port, nodes, levels, variant, q):
