@@ -450,6 +450,16 @@ __device__ __forceinline__ bool is_face(int k) {
   return k == 4 || k == 10 || k == 12 || k == 14 || k == 16 || k == 22;
 }
 
+// tap k = 9 (dz+1) + 3 (dy+1) + (dx+1) by its number of nonzero offsets:
+// 0 centre, 1 face, 2 edge, 3 corner. The binary16 kernels only run on
+// stencils whose faces are zero and whose edge / corner taps are each one
+// value (sym16 in the launcher: every hierarchy level), so they pin three
+// tap registers instead of 21 -- the registers the plane loop needs.
+__host__ __device__ constexpr int tap_class(int k) {
+  return (k / 9 != 1) + ((k / 3) % 3 != 1) + (k % 3 != 1);
+}
+__host__ __device__ constexpr int tap_rep(int c) { return c == 0 ? 13 : (c == 1 ? 4 : (c == 2 ? 1 : 0)); }
+
 // ---- the kernel ----------------------------------------------------------
 // LP storage precision of the stencil operand; CP accumulation precision;
 // EP epilogue/output precision; W values per lane; WX warps per row;
@@ -570,10 +580,11 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
   __shared__ uint32_t s_taps[27];
   if (CP == P16 && tid < 27) s_taps[tid] = h2u(a.t16[tid]);
   __syncthreads();
-  uint32_t tk[27];
+  static_assert(CP != P16 || SKIPF, "binary16 plane kernels take the symmetric (sym16) stencil form");
+  uint32_t tk[4];  // binary16: by tap class (face taps are skipped)
   if constexpr (CP == P16) {
 #pragma unroll
-    for (int k = 0; k < 27; ++k) tk[k] = (SKIPF && is_face(k)) ? 0u : s_taps[k];
+    for (int c = 0; c < 4; ++c) tk[c] = c == 1 ? 0u : s_taps[tap_rep(c)];
   }
   // JACOBI_Z: D^-1 and omega in the compute precision
   const auto jd = [&] {
@@ -588,7 +599,7 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
   }();
   (void)jd; (void)jw;
   auto tapk = [&](int k) {
-    if constexpr (CP == P16) return u2h(tk[k]);
+    if constexpr (CP == P16) return u2h(tk[tap_class(k)]);
     else return tap<CP>(a, k);
   };
 
@@ -610,12 +621,11 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
   double sq = 0.0;
   uint32_t phase = 0;
 
-  // contributions of one operand plane (stage s) to the three output planes
-  // GUARD = false: all three output planes are this CTA's (the hot path);
-  // otherwise u0/u1/u2 select them (first/last two planes of the chunk)
-  auto accumulate = [&](auto guard, const unsigned char* st, bool u0, bool u1, bool u2, Row<CP, W>* A0,
-                        Row<CP, W>* A1, Row<CP, W>* A2) {
-    constexpr bool GUARD = decltype(guard)::value;
+  // contributions of one operand plane (stage s) to the three output planes;
+  // bit d of the compile-time mask M selects output plane A_d (M = 7 on the
+  // interior planes of a chunk, partial masks on its first / last two)
+  auto accumulate = [&](auto mask_c, const unsigned char* st, Row<CP, W>* A0, Row<CP, W>* A1, Row<CP, W>* A2) {
+    constexpr int M = decltype(mask_c)::value;
 #pragma unroll
     for (int j = 0; j < RY + 2; ++j) {
       const unsigned char* rp = st + (tr + j) * K::kXRow;
@@ -648,9 +658,8 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
         for (int dz = 0; dz < 3; ++dz) {
           // operand plane q is dz=+1 for output q-1 (A0), 0 for q (A1), -1 for q+1 (A2)
           Row<CP, W>* Acc = dz == 0 ? A0 : (dz == 1 ? A1 : A2);
-          const bool use = dz == 0 ? u0 : (dz == 1 ? u1 : u2);
           const int tz = 2 - dz;  // tap plane index: dz_tap + 1
-          if (GUARD && !use) continue;
+          if (((M >> dz) & 1) == 0) continue;
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx) {
             const int k = tz * 9 + dyi * 3 + dx;
@@ -765,7 +774,12 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
     }
   };
 
-  // plane loop; the accumulator slots rotate by register moves
+  // plane loop; the accumulator slots rotate by register moves (a 3x unrolled
+  // loop renaming them statically spills at the 128-register cap and measured
+  // slower). Operand plane k feeds output planes q-1 (acc0, ours iff k >= 2),
+  // q (acc1, 1 <= k <= NQ-2) and q+1 (acc2, k <= NQ-3): the chunk's first and
+  // last two planes take statically specialised partial accumulations instead
+  // of per-tap guards.
   for (int k = 0; k < NQ; ++k) {
     const int q = z0 - 1 + k;
     const int s = k % NS;
@@ -774,11 +788,16 @@ __global__ void __launch_bounds__(32 * WX * WY, (CP == P16 && 32 * WX * WY == 12
     if ((q > 0 || a.load_lo) && (q < a.pz || a.load_hi)) {
       mbar_wait(full + s, (phase >> s) & 1u);
       phase ^= 1u << s;
-      // acc0: output q-1 (ours iff k >= 2), acc1: q (1 <= k <= NQ-2), acc2: q+1 (k <= NQ-3)
-      if (k >= 2 && k <= NQ - 3)
-        accumulate(std::false_type{}, st, true, true, true, acc0, acc1, acc2);
-      else
-        accumulate(std::true_type{}, st, k >= 2, k >= 1 && k <= NQ - 2, k <= NQ - 3, acc0, acc1, acc2);
+      const int m = (k >= 2) | (k >= 1 && k <= NQ - 2) << 1 | (k <= NQ - 3) << 2;
+      switch (m) {  // CTA-uniform; mask 5 cannot occur
+        case 7: accumulate(std::integral_constant<int, 7>{}, st, acc0, acc1, acc2); break;
+        case 6: accumulate(std::integral_constant<int, 6>{}, st, acc0, acc1, acc2); break;
+        case 4: accumulate(std::integral_constant<int, 4>{}, st, acc0, acc1, acc2); break;
+        case 3: accumulate(std::integral_constant<int, 3>{}, st, acc0, acc1, acc2); break;
+        case 2: accumulate(std::integral_constant<int, 2>{}, st, acc0, acc1, acc2); break;
+        case 1: accumulate(std::integral_constant<int, 1>{}, st, acc0, acc1, acc2); break;
+        default: break;
+      }
     }
     if (k >= 2) epilogue(stages + ((k - 1) % NS) * K::kStage, q - 1, acc0);
     if constexpr (K::kBReg) {
@@ -833,13 +852,14 @@ __global__ void __launch_bounds__(128) k_direct(const __grid_constant__ PlaneArg
   const int y = 1 + rr % (P - 1), z = 1 + rr / (P - 1);
   const int x0 = lane * W;
   const long long plane = (long long)P * P;
-  uint32_t tk[27];
+  static_assert(LP != P16 || SKIPF, "binary16 direct kernels take the symmetric (sym16) stencil form");
+  uint32_t tk[4];  // binary16: by tap class (see tap_class)
   if constexpr (LP == P16) {
 #pragma unroll
-    for (int k = 0; k < 27; ++k) tk[k] = (SKIPF && is_face(k)) ? 0u : h2u(a.t16[k]);
+    for (int c = 0; c < 4; ++c) tk[c] = c == 1 ? 0u : h2u(a.t16[tap_rep(c)]);
   }
   auto tapk = [&](int k) {
-    if constexpr (LP == P16) return u2h(tk[k]);
+    if constexpr (LP == P16) return u2h(tk[tap_class(k)]);
     else return tap<LP>(a, k);
   };
   const auto jd = [&] {

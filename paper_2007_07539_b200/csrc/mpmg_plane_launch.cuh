@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "mpmg_internal.h"
@@ -225,11 +226,27 @@ inline bool with_pitch(int P, F&& f) {
 
 inline bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
 
-// FP16 stencils may drop the six face taps only when they are exactly zero
-inline bool faces_zero16(const mpmg_stencil& A) {
-  const int f[6] = {4, 10, 12, 14, 16, 22};
-  for (int i : f)
-    if (__half2float(__double2half(A.taps[i])) != 0.0f) return false;
+// the binary16 plane / direct kernels drop the six face taps and keep one
+// value per tap class (tap_class): they run only when, in binary16, the faces
+// are exactly zero and the 12 edge and the 8 corner taps are each one value
+// (true on every level of the hierarchy); anything else takes the stencil
+// kernels
+inline bool sym16(const mpmg_stencil& A) {
+  if (A.ntaps != 27) return false;
+  uint16_t rep[4] = {0, 0, 0, 0};
+  bool seen[4] = {false, false, false, false};
+  for (int k = 0; k < 27; ++k) {
+    const __half h = __double2half(A.taps[k]);
+    uint16_t bits;
+    memcpy(&bits, &h, 2);
+    const int c = tap_class(k);
+    if (c == 1) {
+      if (__half2float(h) != 0.0f) return false;
+      continue;
+    }
+    if (!seen[c]) { seen[c] = true; rep[c] = bits; }
+    else if (rep[c] != bits) return false;
+  }
   return true;
 }
 
@@ -244,7 +261,7 @@ bool plane_level_op_push(int op, const mpmg_stencil& A, const void* x, const voi
                          void* push_hi) {
   if (A.dim != 3 || !slab || (op != 1 && op != 2)) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
-  if (LP == P16 && !faces_zero16(A)) return false;
+  if (LP == P16 && !sym16(A)) return false;
   if (!aligned16(x) || !aligned16(b) || !aligned16(out) || !aligned16(push_lo) || !aligned16(push_hi)) return false;
   PlaneArgs a = plane_args(A, slab);
   a.x = x; a.b = b; a.out = out;
@@ -289,7 +306,7 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
   if (A.dim != 3 || (op != 1 && op != 2 && op != 3)) return false;
   if (pitch(A.nodes) < plane_min_pitch()) return false;
   if (!(policy & MPMG_FMA) || (LP == P16 && (policy & MPMG_ACC32))) return false;
-  if (LP == P16 && !faces_zero16(A)) return false;
+  if (LP == P16 && !sym16(A)) return false;
   if (!aligned16(x) || !aligned16(b) || !aligned16(out)) return false;
   PlaneArgs a = plane_args(A, slab);
   a.x = x; a.b = b; a.out = out;
