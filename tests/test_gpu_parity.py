@@ -227,3 +227,48 @@ def test_final_residual_is_residual_norm(refresh):
     t = O.spmv(cols, vals, FP64, u, O.ctx(False))
     r = b - t
     assert rep.final_residual == pytest.approx(float(np.sqrt(np.dot(r, r))), rel=1e-12)
+
+
+@pytest.mark.parametrize("n", [129, 65])
+def test_asymmetric_binary16_stencil(n, rng):
+    """The binary16 plane / direct kernels keep one register per tap class
+    (sym16): a stencil whose edge taps are not all one value must take the
+    general stencil kernels and still match the oracle bitwise (C ABI defect
+    with one edge tap perturbed; pitch 128 = plane kernel, 64 = direct)."""
+    import ctypes as C
+    import torch
+    Lb = mg.lib()
+    ctx = O.ctx(False, True, False)
+    pol = mg.policy_word(False, True, False)
+    A = mg.level_stencil(3, n, FP16, False)
+    ho = oracle_h(3, n, 2, "h_mg", False)
+    cols, vals = ho.matrix(1, 0)
+    m = n - 2
+    k = 1  # (dz, dy, dx) = (-1, -1, 0): an edge tap
+    off = -m * m - m
+    new = A.taps[k] * 1.5
+    A.taps[k] = new
+    rows = np.arange(cols.shape[0])[:, None]
+    vals = np.where((cols - rows == off) & (vals != 0), O.round_vec([new], FP16, False)[0], vals)
+    N = m ** 3
+    u = rand_level(rng, N, FP16, False, 1e-2)
+    b = rand_level(rng, N, FP16, False, 1.0)
+    plen = Lb.mpmg_padded_len(3, n)
+
+    def pack(x):
+        out = torch.zeros(plen, dtype=torch.float16, device="cuda")
+        src = torch.from_numpy(x).to("cuda").half()
+        mg._check(Lb.mpmg_gpu_pack(3, n, FP16, src.data_ptr(), out.data_ptr(), None), "pack")
+        return out
+
+    ud, bd = pack(u), pack(b)
+    rd = torch.zeros_like(ud)
+    assert Lb.mpmg_gpu_defect(C.byref(A), bd.data_ptr(), ud.data_ptr(), rd.data_ptr(), pol, None) == 0
+    comp = torch.zeros(N, dtype=torch.float16, device="cuda")
+    mg._check(Lb.mpmg_gpu_unpack(3, n, FP16, rd.data_ptr(), comp.data_ptr(), None), "unpack")
+    rg = comp.double().cpu().numpy()
+    ro = O.axpy(FP16, -1.0, O.spmv(cols, vals, FP16, u, ctx), b, ctx)
+    assert same(rg, ro), mismatch(rg, ro)
+    # and the perturbation matters (the symmetric kernels would have ignored it)
+    r0 = O.axpy(FP16, -1.0, O.spmv(*ho.matrix(1, 0), FP16, u, ctx), b, ctx)
+    assert not same(ro, r0)
