@@ -226,6 +226,11 @@ struct Coarse {
   const __half (*t16)[27];
   const float (*t32)[27];
   const bool slab;  // cluster slab mode (else a cooperative grid, level data in global memory)
+  // per-level point geometry and CTA-0 flag, computed once per launch (shared
+  // memory) -- points() divides, and every operation asks several times
+  const Pt* spt = nullptr;
+  const unsigned char* ssmall = nullptr;
+  __device__ const Pt& pt(const CoarseLevel& L) const { return spt[&L - lv]; }
   __device__ Coarse(const CoarseArgs& args, CoarseLevel* table, void* const* cg, const __half (*a16)[27],
                     const float (*a32)[27], bool cluster)
       : a(args), rank(blockIdx.x), ncta(gridDim.x), lv(table), cgp(cg), t16(a16), t32(a32), slab(cluster) {}
@@ -247,7 +252,7 @@ struct Coarse {
 
   template <int PR> using O = Lv<PR, FTZ, FMA, ACC32>;
 
-  __device__ bool small(const CoarseLevel& L) const { return points(L).n <= a.cta_points; }
+  __device__ bool small(const CoarseLevel& L) const { return ssmall[&L - lv] != 0; }
   long long t0 = 0;
   int nst = 0;
   // phase timestamps (MPMG_COARSE_DEBUG): code*1e12 + cycles since start,
@@ -277,7 +282,7 @@ struct Coarse {
   // as for_points_by, with the point's coordinates: f(i, x, y, z, P)
   template <typename F>
   __device__ void for_points_xyz(const CoarseLevel& L, int mode, F&& f) {
-    const Pt p = points(L);
+    const Pt p = pt(L);
     int start = threadIdx.x, stride = blockDim.x, end = p.n;
     if (mode == 1) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
     if (mode == 2) {
@@ -294,7 +299,7 @@ struct Coarse {
   }
   template <typename F>
   __device__ void for_points_by(const CoarseLevel& L, int mode, F&& f) {
-    const Pt p = points(L);
+    const Pt p = pt(L);
     int start = threadIdx.x, stride = blockDim.x, end = p.n;
     if (mode == 1) { start += (int)rank * blockDim.x; stride *= (int)ncta; }
     if (mode == 2) {
@@ -538,8 +543,8 @@ struct Coarse {
   // barriers and shuffles instead of CTA-wide barriers
   template <int PR>
   __device__ void cg(const CoarseLevel& L, const void* bv, void* uv) {
-    if (points(L).n == 1) cg_one<PR>(L, bv, uv);
-    else if (points(L).n <= 32) cg_impl<PR, true>(L, bv, uv);
+    if (pt(L).n == 1) cg_one<PR>(L, bv, uv);
+    else if (pt(L).n <= 32) cg_impl<PR, true>(L, bv, uv);
     else cg_impl<PR, false>(L, bv, uv);
   }
   // cg_impl on a one-unknown base level (every max-depth hierarchy): the
@@ -551,7 +556,7 @@ struct Coarse {
     using OP = O<PR>;
     using T = typename OP::T;
     if (threadIdx.x != 0) return;
-    const Pt pt = points(L);
+    const Pt pt = this->pt(L);
     const int i0 = pt.idx(0);
     const T b = ldcg(static_cast<const T*>(bv) + i0);
     T* uo = static_cast<T*>(uv) + i0;
@@ -606,7 +611,7 @@ struct Coarse {
     T* ap = static_cast<T*>(cgp[2]);
     T* sc = static_cast<T*>(cgp[3]);
     T* best = static_cast<T*>(cgp[4]);
-    const Pt pt = points(L);
+    const Pt pt = this->pt(L);
     auto dot = [&](const T* x, const T* y) -> double {
       if constexpr (WARP) {
         __syncwarp();
@@ -687,6 +692,7 @@ struct Coarse {
       if (a.debug > 1) stamp(8, (int)(&L - lv));
     } else {
       sync(L);
+      if (a.debug > 1) stamp(7, (int)(&L - lv));
     }
   }
 
@@ -808,7 +814,7 @@ struct Coarse {
       if (threadIdx.x == 0) {
         double sc = 1.0;
         if (rescale && in_team(L)) {  // multigrid.cpp:246-250, sequential fma order
-          const Pt pc = points(C);
+          const Pt pc = pt(C);
           double acc = 0.0;
           for (int k = 0; k < pc.n; ++k) {
             const double v = C.prod[pc.idx(k)];
@@ -928,6 +934,12 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
     t32[i / 27][i % 27] = round32<FTZ>(v);
   }
   __shared__ void* cg[5];
+  __shared__ Pt s_pt[kMaxCoarseLevels];
+  __shared__ unsigned char s_small[kMaxCoarseLevels];
+  if (threadIdx.x < a.nlev) {
+    s_pt[threadIdx.x] = points(a.lv[threadIdx.x]);
+    s_small[threadIdx.x] = small_level(a.lv[threadIdx.x], a.cta_points) ? 1 : 0;
+  }
   extern __shared__ __align__(16) unsigned char dyn[];
   if (threadIdx.x == 0) {
     for (int l = 0; l < a.nlev; ++l) table[l] = a.lv[l];
@@ -965,7 +977,10 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
         unsigned char* q[4];
         for (int k = 0; k < 4; ++k) q[k] = dyn + off[l] + k * sz[l];
         if (small_level(a.lv[l], a.cta_points)) {  // CTA 0's full vectors, reached through DSMEM
-          for (int k = 0; k < 4; ++k) q[k] = static_cast<unsigned char*>(cl.map_shared_rank((void*)q[k], 0));
+          // (CTA 0 itself keeps the plain shared-memory addresses: its small-level
+          // operations are latency chains, and a cluster-window access is slower)
+          if (blockIdx.x != 0)
+            for (int k = 0; k < 4; ++k) q[k] = static_cast<unsigned char*>(cl.map_shared_rank((void*)q[k], 0));
         } else {  // virtual base: global plane z of the slab at base + z * plane bytes
           const long long P = a.lv[l].nodes - 1;
           const long long shift = (long long)(slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, blockIdx.x) - 1) *
@@ -1001,6 +1016,8 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
     }
     __syncthreads();
     Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, true);
+    c.spt = s_pt;
+    c.ssmall = s_small;
     c.slo = slo_tab;
     c.push = push_tab;
     c.run_slab();
@@ -1012,6 +1029,8 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
   }
   __syncthreads();
   Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, false);
+  c.spt = s_pt;
+  c.ssmall = s_small;
   c.run();
 }
 
