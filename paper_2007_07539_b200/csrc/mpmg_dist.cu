@@ -50,6 +50,7 @@ constexpr int kMaxWorld = 64;
 struct DState {  // device IR state (ir_solver.cpp:95-120)
   double alpha, scale;
   int iterations, converged, diverged, active, refresh_now, final_pending;
+  int pending, fold_now;  // deferred corrections (as IrState, mpmg_solver.cu)
 };
 
 struct Comm {  // device-resident exchange bookkeeping (part of the arena)
@@ -113,10 +114,12 @@ __global__ void k_publish(Comm* self, Comm* const* peers, int rank, int world, c
 // alpha = sqrt(sum of the ranks' slots in rank order); ir_solver.cpp:95-120
 __global__ void k_dcontrol(DState* st, const Comm* self, int world, double* hist, int hist_cap, double tol,
                            int max_it, int scale_enabled, int refresh, int increment,
-                           cudaGraphConditionalHandle cond, int use_cond) {
+                           cudaGraphConditionalHandle cond, int use_cond, int ring_k) {
   double s = 0.0;
   for (int t = 0; t < world; ++t) s += self->slot[t];
   const double alpha = sqrt(s);
+  // deferred corrections: this iteration parked one more c, or folded them all
+  if (increment && ring_k > 0) st->pending = st->fold_now ? 0 : st->pending + 1;
   if (increment) st->iterations += 1;
   const int it = st->iterations;
   if (hist && it < hist_cap) hist[it] = alpha;
@@ -130,6 +133,8 @@ __global__ void k_dcontrol(DState* st, const Comm* self, int world, double* hist
   }
   st->active = active;
   st->refresh_now = (refresh > 0 && (it + 1) % refresh == 0) ? 1 : 0;
+  // the next iteration folds the ring into u when it refreshes r or fills the ring
+  st->fold_now = ring_k > 0 && (st->refresh_now || st->pending + 1 >= ring_k) ? 1 : 0;
   if (use_cond) cudaGraphSetConditional(cond, active ? 1u : 0u);
 }
 
@@ -137,6 +142,7 @@ __global__ void k_dreset(DState* st) {
   st->alpha = 0.0;
   st->scale = 1.0;
   st->iterations = st->converged = st->diverged = st->active = st->refresh_now = 0;
+  st->pending = st->fold_now = 0;
   st->final_pending = 1;
 }
 
@@ -184,6 +190,13 @@ struct mpmg_dist {
   int *lo_dev = nullptr, *hi_dev = nullptr, *all_dev = nullptr;
   double *partU = nullptr, *partD = nullptr;
   int nU = 0, nD = 0;
+  // deferred corrections (binary16/32 finest level, as mpmg_solver.cu): the
+  // iteration's c is parked in ring slot `pending` by UPDATE_R (r only) and
+  // folded into the owned planes of u at a refresh, a full ring and the end
+  int ring_k = 0;
+  void* ring = nullptr;  // ring_k slots of ring_len values (the finest slab layout)
+  long long ring_len = 0;
+  double* ring_scale = nullptr;
   DState* st = nullptr;
   double* hist = nullptr;
   int hist_cap = 0;
@@ -194,8 +207,9 @@ struct mpmg_dist {
   mpmg_solve_params gkey{};
   bool gvalid = false;
   bool connected = false;
-  bool fuse_halos = true;
-  int n_fused = 0, n_copied = 0;  // halo exchanges recorded in the last graph  // MPMG_DIST_FUSE_HALOS=0: kernel + copy exchange
+  bool fuse_halos = true;         // MPMG_DIST_FUSE_HALOS=0: kernel + copy exchange
+  bool fuse_jz = true;            // MPMG_DIST_JZ=0: pointwise step 1 + stencil step 2
+  int n_fused = 0, n_copied = 0;  // halo exchanges recorded in the last graph
 
   template <typename T = void>
   T* at(size_t off) { return reinterpret_cast<T*>(arena + off); }
@@ -210,7 +224,7 @@ struct mpmg_dist {
     if (coarse) mpmg_solver_destroy(coarse);
     for (int r = 0; r < (int)peer.size(); ++r)
       if (r != rank && peer[r] && peer_ipc[r]) cudaIpcCloseMemHandle(peer[r]);
-    for (void* p : {(void*)arena, (void*)peers_dev, (void*)lo_dev, (void*)hi_dev, (void*)all_dev, (void*)partU,
+    for (void* p : {(void*)ring, (void*)ring_scale, (void*)arena, (void*)peers_dev, (void*)lo_dev, (void*)hi_dev, (void*)all_dev, (void*)partU,
                     (void*)partD, (void*)st, (void*)hist, (void*)final_d})
       if (p) cudaFree(p);
     if (e0) cudaEventDestroy(e0);
@@ -348,9 +362,27 @@ struct mpmg_dist {
       if (rc != MPMG_OK && e == cudaSuccess) e = cudaErrorUnknown;
     };
     if (cfg.pre_steps > 0) {
-      ok(mpmg_gpu_slab_jacobi(&L.A, &L.s, at(L.b), nullptr, at(cur), cfg.omega, policy(), q));
+      int done = 1;  // pre-smoothing steps taken
+      bool jz = false;
+      if (cfg.pre_steps >= 2 && fuse_jz) {
+        // steps 1 + 2 from u = 0 in one JACOBI_Z sweep (u1 = w D^-1 b formed on
+        // the fly from the staged b): needs b's halo planes instead of u1's
+        e = exchange(l, L.b, true, true, q);
+        cudaError_t pe = cudaSuccess;
+        if (e == cudaSuccess) {
+          if (L.prec == MPMG_FP16)
+            jz = plane_level_op_f16(3, L.A, at(L.b), at(L.b), at(cur), cfg.omega, policy(), q, &pe, &L.s);
+          else if (L.prec == MPMG_FP32)
+            jz = plane_level_op_f32(3, L.A, at(L.b), at(L.b), at(cur), cfg.omega, policy(), q, &pe, &L.s);
+          else
+            jz = plane_level_op_f64(3, L.A, at(L.b), at(L.b), at(cur), cfg.omega, policy(), q, &pe, &L.s);
+          if (jz) e = pe;
+        }
+        if (jz) done = 2;
+      }
+      if (!jz && e == cudaSuccess) ok(mpmg_gpu_slab_jacobi(&L.A, &L.s, at(L.b), nullptr, at(cur), cfg.omega, policy(), q));
       if (e == cudaSuccess) e = exchange(l, cur, true, true, q);
-      for (int k = 1; k < cfg.pre_steps && e == cudaSuccess; ++k) {
+      for (int k = done; k < cfg.pre_steps && e == cudaSuccess; ++k) {
         e = op_push(2, l, L.b, cur, other, true, true, q);
         std::swap(cur, other);
       }
@@ -392,7 +424,8 @@ struct mpmg_dist {
     }
     if (e == cudaSuccess) {
       k_dcontrol<<<1, 1, 0, q>>>(st, comm(), world, hist, hist_cap, p.outer_tolerance, p.max_outer_iterations,
-                                 scale_enabled(p), p.residual_refresh_interval, increment ? 1 : 0, h, use_cond);
+                                 scale_enabled(p), p.residual_refresh_interval, increment ? 1 : 0, h, use_cond,
+                                 ring_k);
       e = cudaGetLastError();
     }
     return e;
@@ -415,16 +448,27 @@ struct mpmg_dist {
                                 int use_cond) {
     DLevel& F = lv[top];
     cudaError_t e = cudaSuccess;
-    // cast_vector(r, mg precision, scale) over the local slab (ir_solver.cpp:109-110)
-    if (mpmg_gpu_slab_scale_downcast(F.P + 1, &F.s, at<double>(off_r), at(F.b), F.prec, &st->scale, 1, policy(),
-                                     q) != MPMG_OK)
-      return cudaErrorUnknown;
+    // cast_vector(r, mg precision, scale) over the owned planes (ir_solver.cpp:109-110;
+    // b's halo planes belong to the neighbours' exchanges)
+    {
+      const size_t pl = (size_t)F.P * F.P;
+      e = launch_downcast_len((size_t)F.s.nz * pl, at<double>(off_r) + pl, at<unsigned char>(F.b) + pl * F.bytes,
+                              F.prec, &st->scale, 1, policy(), q);
+      if (e != cudaSuccess) return e;
+    }
     size_t c = 0;
     e = cycle(top, q, &c);
     // update_residuum_correction (ir_solver.cpp:112): c's halos are exchanged
-    if (e == cudaSuccess && mpmg_gpu_slab_update_rc(&A64, &F.s, at(c), F.prec, at<double>(off_r), at<double>(off_u),
-                                                    &st->scale, partU, policy(), q) != MPMG_OK)
+    if (ring_k > 0) {  // r -= a A c now, u += a c deferred (bitwise the same u)
+      if (e == cudaSuccess && !plane_update_r(A64, at(c), F.prec, at<double>(off_r), &st->scale, partU, ring,
+                                              ring_len, &st->pending, ring_scale, fma(), q, &e, &F.s))
+        e = cudaErrorNotSupported;
+      if (e == cudaSuccess) e = fold(1, &st->fold_now, q);
+    } else if (e == cudaSuccess && mpmg_gpu_slab_update_rc(&A64, &F.s, at(c), F.prec, at<double>(off_r),
+                                                           at<double>(off_u), &st->scale, partU, policy(),
+                                                           q) != MPMG_OK) {
       e = cudaErrorUnknown;
+    }
     // the refresh r = b - A u every refresh-th iteration (ir_solver.cpp:115-119),
     // gated on the device; u's halos first
     if (e == cudaSuccess && p.residual_refresh_interval > 0) {
@@ -439,9 +483,20 @@ struct mpmg_dist {
     return e;
   }
 
+  // the parked corrections (+ this iteration's when extra = 1) into u's owned
+  // planes only: a neighbour may be storing into u's halo planes meanwhile
+  cudaError_t fold(int extra, const int* gate, cudaStream_t q) {
+    const DLevel& F = lv[top];
+    const size_t pl = (size_t)F.P * F.P;
+    return launch_fold((size_t)F.s.nz * pl, at<double>(off_u) + pl,
+                       static_cast<unsigned char*>(ring) + pl * bytes_of(F.prec), ring_len, F.prec, ring_scale,
+                       &st->pending, extra, gate, fma(), q);
+  }
+
   cudaError_t enqueue_final(cudaStream_t q) {  // residual_norm (ir_solver.cpp:21-49)
     const DLevel& F = lv[top];
-    cudaError_t e = exchange(top, off_u, true, true, q, 8);
+    cudaError_t e = ring_k > 0 ? fold(0, nullptr, q) : cudaSuccess;  // corrections still parked
+    if (e == cudaSuccess) e = exchange(top, off_u, true, true, q, 8);
     if (e == cudaSuccess && mpmg_gpu_slab_defect_f64(&A64, &F.s, at<double>(off_b), at<double>(off_u), nullptr,
                                                      partD, 1, q) != MPMG_OK)
       e = cudaErrorUnknown;
@@ -550,6 +605,7 @@ mpmg_dist* mpmg_dist_create(const mpmg_solver_config* cfg, int32_t rank, int32_t
   auto* D = new mpmg_dist();
   D->cfg = c;
   if (const char* fe = std::getenv("MPMG_DIST_FUSE_HALOS")) D->fuse_halos = std::atoi(fe) != 0;
+  if (const char* je = std::getenv("MPMG_DIST_JZ")) D->fuse_jz = std::atoi(je) != 0;
   D->rank = rank;
   D->world = world;
   D->levels = c.levels;
@@ -606,6 +662,21 @@ mpmg_dist* mpmg_dist_create(const mpmg_solver_config* cfg, int32_t rank, int32_t
   const DLevel& F = D->lv[D->top];
   D->nU = std::max(1, mpmg_gpu_slab_partials_len(c.nodes, &F.s, F.prec, 1));
   D->nD = std::max(1, mpmg_gpu_slab_partials_len(c.nodes, &F.s, F.prec, 0));
+  if (F.prec != MPMG_FP64) {
+    const char* de = std::getenv("MPMG_DEFER_U");
+    const int nr = (de && std::atoi(de) == 0) ? -1 : plane_update_r_partials(3, c.nodes, F.prec, F.s.nz + 1);
+    if (nr > 0) {
+      D->ring_k = 10;
+      D->nU = nr;
+      D->ring_len = (long long)((F.slab_len + 63) / 64 * 64);
+    }
+  }
+  if (e == cudaSuccess && D->ring_k > 0) {
+    const size_t rb = (size_t)D->ring_k * (size_t)D->ring_len * (size_t)F.bytes;
+    e = cudaMalloc(&D->ring, rb);
+    if (e == cudaSuccess) e = cudaMemset(D->ring, 0, rb);
+    if (e == cudaSuccess) e = cudaMalloc(&D->ring_scale, (size_t)D->ring_k * 8);
+  }
   const int np = std::max(D->nU, D->nD);
   if (e == cudaSuccess) e = cudaMalloc(&D->partU, np * 8);
   if (e == cudaSuccess) e = cudaMalloc(&D->partD, np * 8);
@@ -746,7 +817,6 @@ int mpmg_dist_solve_device(mpmg_dist* D, const mpmg_solve_params* pp, double* hi
   if (!D || !D->connected || !pp || !(pp->outer_tolerance > 0.0) || pp->max_outer_iterations < 0 ||
       pp->random_initial_guess)
     return MPMG_EINVAL;
-  const mpmg_solve_params p = *pp;
   // (re)building the graph allocates and may synchronize the device: done
   // here only if the caller did not prepare this solve
   const int prc = mpmg_dist_prepare(D, pp);

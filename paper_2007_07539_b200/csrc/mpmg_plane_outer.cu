@@ -86,11 +86,11 @@ bool plane_update_rc(const mpmg_stencil& A64, const void* c, int c_prec, double*
 // u += a c, see mpmg_solver.cu); binary16/32 c only
 bool plane_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* r, const double* alpha_dev,
                     double* partials, void* ring, long long ring_len, const int* slot, double* ring_scale, bool fma,
-                    cudaStream_t s, cudaError_t* err) {
+                    cudaStream_t s, cudaError_t* err, const mpmg_slab* slab) {
   if (c_prec == MPMG_FP64 || !plane_outer_supported(A64.dim, A64.nodes) || !aligned16(c) || !aligned16(r) ||
       !aligned16(ring) || (ring_len * mpmg_bytes_per_value(c_prec)) % 16 != 0)
     return false;
-  PlaneArgs a = plane_args(A64);
+  PlaneArgs a = plane_args(A64, slab);
   a.x = c; a.r64 = r; a.alpha = alpha_dev; a.partials = partials;
   a.ring = ring; a.ring_len = ring_len; a.ring_slot = slot; a.ring_scale = ring_scale;
   return with_pitch(a.P, [&](auto pc) {
@@ -105,13 +105,14 @@ bool plane_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* 
   });
 }
 
-int plane_update_r_partials(int dim, int nodes, int lp) {
+int plane_update_r_partials(int dim, int nodes, int lp, int pz) {
   if (!plane_outer_supported(dim, nodes) || lp == MPMG_FP64) return -1;
   int n = -1;
+  if (pz <= 0) pz = pitch(nodes);
   with_pitch(pitch(nodes), [&](auto pc) {
     constexpr int PP = decltype(pc)::value;
-    n = lp == MPMG_FP16 ? PlaneLaunch<P16, P64, P64, POP_UPDATE_R, false, true, PP, OV>::partials()
-                        : PlaneLaunch<P32, P64, P64, POP_UPDATE_R, false, true, PP, OV>::partials();
+    n = lp == MPMG_FP16 ? PlaneLaunch<P16, P64, P64, POP_UPDATE_R, false, true, PP, OV>::partials(pz)
+                        : PlaneLaunch<P32, P64, P64, POP_UPDATE_R, false, true, PP, OV>::partials(pz);
   });
   return n;
 }

@@ -84,13 +84,17 @@ def test_dist_matches_single_gpu(variant, world):
 @pytest.mark.parametrize("variant", ["h_mg", "d_mg"])
 def test_dist_fused_halos_match_copy_exchange(variant, monkeypatch):
     """the halo planes stored into the neighbours' memory by the producing
-    Jacobi / defect kernel (default) and the kernel + peer-copy exchange
-    (MPMG_DIST_FUSE_HALOS=0) give the identical solve, bit for bit"""
+    Jacobi / defect kernel and the fused JACOBI_Z pre-smoothing sweep (both
+    default) against the kernel + peer-copy exchange and pointwise step 1 +
+    stencil step 2 (MPMG_DIST_FUSE_HALOS=0, MPMG_DIST_JZ=0): the identical
+    solve, bit for bit"""
     nodes, levels, world = 257, 8, 4
     monkeypatch.setenv("MPMG_DIST_FUSE_HALOS", "0")
+    monkeypatch.setenv("MPMG_DIST_JZ", "0")
     out0, u0, _, _ = run_ranks(nodes, levels, variant, world)
     assert all(f == 0 and c > 0 for f, c in run_ranks.stats)
     monkeypatch.setenv("MPMG_DIST_FUSE_HALOS", "1")
+    monkeypatch.setenv("MPMG_DIST_JZ", "1")
     out1, u1, _, _ = run_ranks(nodes, levels, variant, world)
     # the slab Jacobi sweeps and defects of pitch 256 and 128 fused
     assert all(f > 0 for f, _ in run_ranks.stats), run_ranks.stats
