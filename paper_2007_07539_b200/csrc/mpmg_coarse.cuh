@@ -365,7 +365,9 @@ struct Coarse {
     using OP = O<P16>;
     const int l = (int)(&L - lv);
     const int P = L.nodes - 1, P2 = P * P, hp = P / 2;
-    const int zlo = lo(l, (int)rank), nz = lo(l, (int)rank + 1) - zlo;
+    // a slab level: this CTA's planes; a CTA-0 level (in CTA 0's shared memory): all
+    const bool whole = small(L);
+    const int zlo = whole ? 1 : lo(l, (int)rank), nz = whole ? P - 1 : lo(l, (int)rank + 1) - zlo;
     const int np = (P - 1) * hp;  // pairs per plane
     // 32-bit shared-window addresses of the virtual bases (global plane z at
     // base + 2 z P^2; modular arithmetic, only in-slab addresses are formed)
@@ -387,9 +389,10 @@ struct Coarse {
     const __half2 m1 = u2h(0xBC00BC00u);
     const __half2 w = __half2half2(OP::from(L.omega)), d = __half2half2(OP::from(L.inv_diag));
     const __half2 z2 = u2h(0u);
-    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    for (int t = threadIdx.x; t < np * nz; t += blockDim.x) {  // (pair, plane) items
+      const int zq = t / np, k = t - zq * np;
       const int y = 1 + k / hp, x = 2 * (k - (y - 1) * hp);
-      for (int zq = 0; zq < nz; ++zq) {
+      {
         const uint32_t off = 2u * (uint32_t)((zlo + zq) * P2 + y * P + x);
         __half2 acc = z2, uc = z2;
         if (DEF || !from_zero) {
@@ -417,8 +420,10 @@ struct Coarse {
       }
     }
   }
+  // slab mode: every 3D level with an even pitch -- slab levels, and CTA 0's
+  // levels (whose buffers CTA 0 addresses as plain shared memory)
   __device__ bool pairs_ok(const CoarseLevel& L) const {
-    return slab && !small(L) && L.dim == 3 && ((L.nodes - 1) & 1) == 0;
+    return slab && (!small(L) || rank == 0) && L.dim == 3 && ((L.nodes - 1) & 1) == 0;
   }
 
   template <int PR>
@@ -1041,6 +1046,8 @@ cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kThreads);
   cfg.stream = s;
+  // (no programmatic dependent launch: measured, an early-resident 16-CTA
+  // cluster slows the FP64 cascade's predecessors by ~60 us per V-cycle)
   cudaLaunchAttribute at[1];
   cfg.attrs = at;
   cfg.numAttrs = 1;
