@@ -734,7 +734,8 @@ struct Coarse {
   __device__ void run_slab() {
     void* cur[kMaxCoarseLevels];
     const int top = a.nlev - 1;
-    t0 = clock64();
+    if (t0 == 0) t0 = clock64();
+    stamp(10, 0);    // (debug: t0 = kernel entry, so this is the set-up time)
     cluster_sync();  // every CTA's shared memory is laid out and zeroed
     copy_level(lv[top], a.lv[top].b, lv[top].b);  // own planes of the top rhs
     __syncthreads();
@@ -782,6 +783,7 @@ struct Coarse {
       stamp(3, l);
     }
     copy_level(lv[top], cur[top], a.lv[top].u);  // own planes of the top correction
+    stamp(12, top);
     stamps_done();
   }
 
@@ -930,6 +932,7 @@ __host__ __device__ inline size_t slab_smem(const CoarseArgs& a, int C, size_t* 
 
 template <bool FTZ, bool FMA, bool ACC32, int UP>
 __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ CoarseArgs a, int use_smem, int cluster) {
+  const long long t_entry = a.dbg ? clock64() : 0;
   __shared__ CoarseLevel table[kMaxCoarseLevels];
   __shared__ __half t16[kMaxCoarseLevels][27];
   __shared__ float t32[kMaxCoarseLevels][27];
@@ -946,8 +949,13 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
     s_small[threadIdx.x] = small_level(a.lv[threadIdx.x], a.cta_points) ? 1 : 0;
   }
   extern __shared__ __align__(16) unsigned char dyn[];
+  // level table: a parallel word copy of the launch parameters (a serial
+  // struct copy by one thread cost microseconds); pointers patched below
+  static_assert(sizeof(CoarseLevel) % 8 == 0, "");
+  for (int i = threadIdx.x; i < a.nlev * (int)(sizeof(CoarseLevel) / 8); i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(table)[i] = reinterpret_cast<const unsigned long long*>(a.lv)[i];
+  __syncthreads();
   if (threadIdx.x == 0) {
-    for (int l = 0; l < a.nlev; ++l) table[l] = a.lv[l];
     cg[0] = a.cg_r; cg[1] = a.cg_p; cg[2] = a.cg_ap; cg[3] = a.cg_s; cg[4] = a.cg_best;
     if (use_smem && blockIdx.x == 0) {
       unsigned char* p = dyn;
@@ -973,11 +981,12 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
       const int T = a.nlev - 1, l = i / 17, r = i % 17;
       slo_tab[l][r] = (short)(r <= (int)gridDim.x ? slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, r) : 0);
     }
+    __syncthreads();  // slo_tab
     if (threadIdx.x == 0) {
-      size_t off[kMaxCoarseLevels + 1], sz[kMaxCoarseLevels];
-      slab_smem(a, (int)gridDim.x, off, sz);
+      // layout from the launcher (slab_smem on the host: no per-CTA division loops)
+      const unsigned long long* off = a.slab_off;
+      const unsigned long long* sz = a.slab_sz;
       cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-      const int T = a.nlev - 1;
       for (int l = 0; l < a.nlev; ++l) {
         unsigned char* q[4];
         for (int k = 0; k < 4; ++k) q[k] = dyn + off[l] + k * sz[l];
@@ -988,8 +997,7 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
             for (int k = 0; k < 4; ++k) q[k] = static_cast<unsigned char*>(cl.map_shared_rank((void*)q[k], 0));
         } else {  // virtual base: global plane z of the slab at base + z * plane bytes
           const long long P = a.lv[l].nodes - 1;
-          const long long shift = (long long)(slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, blockIdx.x) - 1) *
-                                  P * P * bytes_of(a.lv[l].prec);
+          const long long shift = (long long)(slo_tab[l][blockIdx.x] - 1) * P * P * bytes_of(a.lv[l].prec);
           for (int k = 0; k < 4; ++k) q[k] -= shift;
         }
         table[l].u = q[0]; table[l].u2 = q[1]; table[l].b = q[2]; table[l].r = q[3];
@@ -997,7 +1005,7 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
       const size_t b0 = (padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16;
       for (int k = 0; k < 5; ++k) cg[k] = dyn + off[a.nlev] + k * b0;
     }
-    const size_t n = slab_smem(a, (int)gridDim.x, nullptr, nullptr) / 16;
+    const size_t n = a.slab_total / 16;
     for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     if (threadIdx.x < a.nlev) {  // push tables
@@ -1025,6 +1033,7 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
     c.ssmall = s_small;
     c.slo = slo_tab;
     c.push = push_tab;
+    c.t0 = t_entry;
     c.run_slab();
     return;
   }
@@ -1100,7 +1109,12 @@ cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
       at[0].val.clusterDim.x = c;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
-      return cudaLaunchKernelEx(&cfg, kern, a, 1, c);
+      CoarseArgs ac = a;
+      size_t off[kMaxCoarseLevels + 1], sz[kMaxCoarseLevels];
+      ac.slab_total = slab_smem(a, c, off, sz);
+      for (int l = 0; l <= a.nlev; ++l) ac.slab_off[l] = off[l];
+      for (int l = 0; l < a.nlev; ++l) ac.slab_sz[l] = sz[l];
+      return cudaLaunchKernelEx(&cfg, kern, ac, 1, c);
     }
   }
   const size_t smem = coarse_smem(a);

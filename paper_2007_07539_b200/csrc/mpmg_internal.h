@@ -158,6 +158,8 @@ struct CoarseArgs {
   int cta_points;      // levels with <= this many unknowns run on CTA 0 out of shared memory
   int debug;           // MPMG_COARSE_DEBUG=1: record per-phase clock64 stamps
   long long* dbg;      // device buffer for them (64 entries) or nullptr
+  // cluster slab mode shared-memory layout, filled by the launcher (slab_smem)
+  unsigned long long slab_off[kMaxCoarseLevels + 1], slab_sz[kMaxCoarseLevels], slab_total;
 };
 cudaError_t launch_coarse_cycle(const CoarseArgs& a, uint32_t policy, cudaStream_t s);
 

@@ -26,7 +26,8 @@ rc = lib.mpmg_solver_coarse_debug(h.handle, buf, 64)
 assert rc == 0, rc
 cnt = buf[0]
 prev = 0
-names = {1: "down", 2: "base", 3: "up", 4: " pre", 5: " def", 6: " pro", 7: "  cmp", 8: "  xch", 9: "  psh"}
+names = {1: "down", 2: "base", 3: "up", 4: " pre", 5: " def", 6: " pro", 7: "  cmp", 8: "  xch", 9: "  psh",
+         10: "setup", 12: "out"}
 print(f"{variant} {n}^3 L={L}: {cnt} stamps (cycles @ ~1.9 GHz)")
 for i in range(1, cnt + 1):
     code, cyc = divmod(buf[i], 1000000000000)
