@@ -954,10 +954,17 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
   static_assert(sizeof(CoarseLevel) % 8 == 0, "");
   for (int i = threadIdx.x; i < a.nlev * (int)(sizeof(CoarseLevel) / 8); i += blockDim.x)
     reinterpret_cast<unsigned long long*>(table)[i] = reinterpret_cast<const unsigned long long*>(a.lv)[i];
+  __shared__ short slo_tab[kMaxCoarseLevels][17];
+  __shared__ PushTab push_tab[kMaxCoarseLevels];
+  if (cluster)  // slab mode: plane ownership of every level and CTA
+    for (int i = threadIdx.x; i < a.nlev * 17; i += blockDim.x) {
+      const int T = a.nlev - 1, l = i / 17, r = i % 17;
+      slo_tab[l][r] = (short)(r <= (int)gridDim.x ? slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, r) : 0);
+    }
   __syncthreads();
   if (threadIdx.x == 0) {
     cg[0] = a.cg_r; cg[1] = a.cg_p; cg[2] = a.cg_ap; cg[3] = a.cg_s; cg[4] = a.cg_best;
-    if (use_smem && blockIdx.x == 0) {
+    if (use_smem && blockIdx.x == 0 && !cluster) {
       unsigned char* p = dyn;
       for (int l = 0; l < a.nlev; ++l) {
         if (!small_level(a.lv[l], a.cta_points)) continue;
@@ -973,44 +980,34 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
       }
     }
   }
-  __syncthreads();
-  __shared__ short slo_tab[kMaxCoarseLevels][17];
-  __shared__ PushTab push_tab[kMaxCoarseLevels];
   if (cluster) {  // slab mode: every CTA lays out its slabs (and CTA 0's levels)
-    for (int i = threadIdx.x; i < a.nlev * 17; i += blockDim.x) {
-      const int T = a.nlev - 1, l = i / 17, r = i % 17;
-      slo_tab[l][r] = (short)(r <= (int)gridDim.x ? slab_lo((int)(a.lv[T].nodes - 1), (int)gridDim.x, T - l, r) : 0);
-    }
-    __syncthreads();  // slo_tab
-    if (threadIdx.x == 0) {
-      // layout from the launcher (slab_smem on the host: no per-CTA division loops)
-      const unsigned long long* off = a.slab_off;
-      const unsigned long long* sz = a.slab_sz;
-      cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-      for (int l = 0; l < a.nlev; ++l) {
-        unsigned char* q[4];
-        for (int k = 0; k < 4; ++k) q[k] = dyn + off[l] + k * sz[l];
-        if (small_level(a.lv[l], a.cta_points)) {  // CTA 0's full vectors, reached through DSMEM
-          // (CTA 0 itself keeps the plain shared-memory addresses: its small-level
-          // operations are latency chains, and a cluster-window access is slower)
-          if (blockIdx.x != 0)
-            for (int k = 0; k < 4; ++k) q[k] = static_cast<unsigned char*>(cl.map_shared_rank((void*)q[k], 0));
-        } else {  // virtual base: global plane z of the slab at base + z * plane bytes
-          const long long P = a.lv[l].nodes - 1;
-          const long long shift = (long long)(slo_tab[l][blockIdx.x] - 1) * P * P * bytes_of(a.lv[l].prec);
-          for (int k = 0; k < 4; ++k) q[k] -= shift;
+    // (one set-up phase: level buffers by thread l, push tables by thread 32 + l,
+    // zero fill by everyone -- the launcher computed the layout)
+    if (threadIdx.x < a.nlev) {
+      const int l = threadIdx.x;
+      unsigned char* q[4];
+      for (int k = 0; k < 4; ++k) q[k] = dyn + a.slab_off[l] + k * a.slab_sz[l];
+      if (small_level(a.lv[l], a.cta_points)) {  // CTA 0's full vectors, reached through DSMEM
+        // (CTA 0 itself keeps the plain shared-memory addresses: its small-level
+        // operations are latency chains, and a cluster-window access is slower)
+        if (blockIdx.x != 0) {
+          cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+          for (int k = 0; k < 4; ++k) q[k] = static_cast<unsigned char*>(cl.map_shared_rank((void*)q[k], 0));
         }
-        table[l].u = q[0]; table[l].u2 = q[1]; table[l].b = q[2]; table[l].r = q[3];
+      } else {  // virtual base: global plane z of the slab at base + z * plane bytes
+        const long long P = a.lv[l].nodes - 1;
+        const long long shift = (long long)(slo_tab[l][blockIdx.x] - 1) * P * P * bytes_of(a.lv[l].prec);
+        for (int k = 0; k < 4; ++k) q[k] -= shift;
       }
-      const size_t b0 = (padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16;
-      for (int k = 0; k < 5; ++k) cg[k] = dyn + off[a.nlev] + k * b0;
-    }
-    const size_t n = a.slab_total / 16;
-    for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    if (threadIdx.x < a.nlev) {  // push tables
-      const int l = threadIdx.x, C = (int)gridDim.x, r = blockIdx.x;
-      PushTab pt{};
+      table[l].u = q[0]; table[l].u2 = q[1]; table[l].b = q[2]; table[l].r = q[3];
+      if (l == 0) {
+        const size_t b0 = (padded_of(a.lv[0]) * bytes_of(a.lv[0].prec) + 15) / 16 * 16;
+        for (int k = 0; k < 5; ++k) cg[k] = dyn + a.slab_off[a.nlev] + k * b0;
+      }
+    } else if (threadIdx.x >= 32 && threadIdx.x < 32 + a.nlev) {  // push tables
+      const int l = threadIdx.x - 32, C = (int)gridDim.x, r = blockIdx.x;
+      PushTab& pt = push_tab[l];
+      int n = 0;
       const int zlo = slo_tab[l][r], zhi = slo_tab[l][r + 1];
       if (!small_level(a.lv[l], a.cta_points))
         for (int t = 0; t < C; ++t) {
@@ -1018,15 +1015,17 @@ __global__ void __launch_bounds__(kThreads) k_coarse(const __grid_constant__ Coa
           const int tlo = slo_tab[l][t], thi = slo_tab[l][t + 1];
           for (int side = 0; side < 2; ++side) {
             const int z = side == 0 ? tlo - 1 : thi;
-            if (z < zlo || z >= zhi || pt.n >= 8) continue;
-            pt.t[pt.n] = (signed char)t;
-            pt.src[pt.n] = (signed char)(z - (zlo - 1));
-            pt.dst[pt.n] = (signed char)(z - (tlo - 1));
-            ++pt.n;
+            if (z < zlo || z >= zhi || n >= 8) continue;
+            pt.t[n] = (signed char)t;
+            pt.src[n] = (signed char)(z - (zlo - 1));
+            pt.dst[n] = (signed char)(z - (tlo - 1));
+            ++n;
           }
         }
-      push_tab[l] = pt;
+      pt.n = n;
     }
+    const size_t n = a.slab_total / 16;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<uint4*>(dyn)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     Coarse<FTZ, FMA, ACC32, UP> c(a, table, cg, t16, t32, true);
     c.spt = s_pt;
