@@ -1066,14 +1066,17 @@ cudaError_t launch_u(const CoarseArgs& a, cudaStream_t s) {
       attr_set = bytes;
     }
   };
-  // slab mode: one cluster (16, else 8 CTAs) when every level is 3D, of one
-  // precision, without DSH rescaling, and the base level is a CTA-0 level
-  static int cl_env = -1;
+  // slab mode: one cluster (16, else 8 CTAs) when every level is 3D, without
+  // DSH rescaling (its restriction norm spans the cluster), and the base level
+  // is a CTA-0 level; mixed cascades (HSD) too unless MPMG_COARSE_MIXED_SLAB=0
+  static int cl_env = -1, mixed_env = -1;
   if (cl_env < 0) {
     const char* e = std::getenv("MPMG_COARSE_CLUSTER");
     cl_env = e ? std::atoi(e) : 16;
+    const char* m = std::getenv("MPMG_COARSE_MIXED_SLAB");
+    mixed_env = m ? std::atoi(m) : 1;
   }
-  bool slab_ok = cl_env > 1 && UP < 3 && !a.rescale && !small_level(T, a.cta_points) &&
+  bool slab_ok = cl_env > 1 && (UP < 3 || mixed_env != 0) && !a.rescale && !small_level(T, a.cta_points) &&
                  small_level(a.lv[0], a.cta_points);
   for (int l = 0; l < a.nlev && slab_ok; ++l) slab_ok = a.lv[l].dim == 3 && a.lv[l].nodes - 1 >= 2;
   if (slab_ok) {
