@@ -318,11 +318,24 @@ struct Coarse {
     const CoarseLevel& L = lv[l];
     const int P = L.nodes - 1;
     const int bytes = L.prec == MPMG_FP16 ? 2 : (L.prec == MPMG_FP32 ? 4 : 8);
-    const int pl = P * P * bytes;  // plane bytes (a multiple of 16)
+    const int pl = P * P * bytes;  // plane bytes: a multiple of 8 (P is even on a slab level)
     const int zlo = lo(l, (int)rank);
     __syncthreads();
     const int cnt = push[l].n;
-    if (cnt > 0) {
+    if (cnt > 0 && (pl & 15) != 0) {  // binary16 with P = 2 mod 4: 8-byte words
+      const uint32_t real = (uint32_t)__cvta_generic_to_shared(static_cast<unsigned char*>(x) + (long long)(zlo - 1) * pl);
+      const int n8 = pl / 8;
+      for (int i = threadIdx.x; i < cnt * n8; i += blockDim.x) {
+        const int k = i / n8, c = i - k * n8;
+        uint32_t dst;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(dst) : "r"(real + (uint32_t)push[l].dst[k] * (uint32_t)pl), "r"((int)push[l].t[k]));
+        uint2 v;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                     : "=r"(v.x), "=r"(v.y) : "r"(real + (uint32_t)push[l].src[k] * (uint32_t)pl + 8u * c));
+        asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" :: "r"(dst + 8u * c), "r"(v.x), "r"(v.y) : "memory");
+      }
+    } else if (cnt > 0) {
       // shared-window addresses: ld.shared locally, st.shared::cluster remotely
       const uint32_t real = (uint32_t)__cvta_generic_to_shared(static_cast<unsigned char*>(x) + (long long)(zlo - 1) * pl);
       const int n16 = pl / 16;
