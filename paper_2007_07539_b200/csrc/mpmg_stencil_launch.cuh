@@ -3,6 +3,7 @@
 // policy-templated instantiations compile in parallel.
 #pragma once
 
+#include <algorithm>
 #include <type_traits>
 
 #include "mpmg_internal.h"
@@ -37,8 +38,22 @@ inline StencilArgs make_args(const mpmg_stencil& A, int zc) {
 template <int DIM, int LP, int CP, int EP, int OP, bool FTZ, bool FMA>
 cudaError_t run_stencil(const StencilArgs& a, cudaStream_t s) {
   using G = Geo<LP, CP>;
-  const dim3 grid = stencil_grid(DIM, a.P, G::W, G::RY, G::BW, G::ZC);
   const dim3 block(32, G::BW);
+  if constexpr (!OpTraits<OP>::kNorm && DIM == 3) {
+    // level ops on pitches the plane kernels do not take (not a power of two:
+    // 192, 96, 48, ...): z-chunks short enough for about four CTAs per SM --
+    // the fixed 16-plane chunks left 9 to 288 CTAs at these sizes. (The norm
+    // ops keep ZC: their partial-sum count is sized from it.)
+    const dim3 g0 = stencil_grid(DIM, a.P, G::W, G::RY, G::BW, G::ZC);
+    const long long xy = (long long)g0.x * g0.y, target = 4LL * 148;
+    int zc = (int)std::min<long long>(G::ZC, std::max<long long>(1, (long long)(a.P - 1) * xy / target));
+    StencilArgs b = a;
+    b.zc = zc;
+    const dim3 grid = stencil_grid(DIM, a.P, G::W, G::RY, G::BW, zc);
+    k_stencil<DIM, LP, CP, EP, OP, FTZ, FMA, G::RY, G::BW><<<grid, block, 0, s>>>(b);
+    return cudaGetLastError();
+  }
+  const dim3 grid = stencil_grid(DIM, a.P, G::W, G::RY, G::BW, G::ZC);
   k_stencil<DIM, LP, CP, EP, OP, FTZ, FMA, G::RY, G::BW><<<grid, block, 0, s>>>(a);
   return cudaGetLastError();
 }
