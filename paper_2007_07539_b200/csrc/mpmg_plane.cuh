@@ -152,32 +152,42 @@ __device__ __forceinline__ void rload(const unsigned char* s, Row<CP, W>& r) {
   if constexpr (SP == P16) {
     if constexpr (CP == P16) {
       if constexpr (W == 1) r.h = *reinterpret_cast<const __half*>(s);
-      else if constexpr (W == 2) r.h[0] = u2h(*reinterpret_cast<const uint32_t*>(s));
-      else if constexpr (W == 4) {
-        const uint2 q = *reinterpret_cast<const uint2*>(s);
-        r.h[0] = u2h(q.x); r.h[1] = u2h(q.y);
-      } else {
+      else if constexpr (W % 8 == 0) {
 #pragma unroll
         for (int i = 0; i < W / 8; ++i) {
           const uint4 q = *reinterpret_cast<const uint4*>(s + 16 * i);
           r.h[4 * i + 0] = u2h(q.x); r.h[4 * i + 1] = u2h(q.y); r.h[4 * i + 2] = u2h(q.z); r.h[4 * i + 3] = u2h(q.w);
         }
+      } else if constexpr (W % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < W / 4; ++i) {
+          const uint2 q = *reinterpret_cast<const uint2*>(s + 8 * i);
+          r.h[2 * i] = u2h(q.x); r.h[2 * i + 1] = u2h(q.y);
+        }
+      } else {  // W = 2, 6: 4-byte words (a lane's row segment is only 4-byte aligned)
+#pragma unroll
+        for (int i = 0; i < W / 2; ++i) r.h[i] = u2h(*reinterpret_cast<const uint32_t*>(s + 4 * i));
       }
     } else {  // widen (exact)
       const __half* hp = reinterpret_cast<const __half*>(s);
       if constexpr (W == 1) r.v[0] = (typename Sc<CP>::T)__half2float(hp[0]);
       else {
         __half2 tmp[W / 2];
-        if constexpr (W == 2) tmp[0] = u2h(*reinterpret_cast<const uint32_t*>(s));
-        else if constexpr (W == 4) {
-          const uint2 q = *reinterpret_cast<const uint2*>(s);
-          tmp[0] = u2h(q.x); tmp[1] = u2h(q.y);
-        } else {
+        if constexpr (W % 8 == 0) {
 #pragma unroll
           for (int i = 0; i < W / 8; ++i) {
             const uint4 q = *reinterpret_cast<const uint4*>(s + 16 * i);
             tmp[4 * i + 0] = u2h(q.x); tmp[4 * i + 1] = u2h(q.y); tmp[4 * i + 2] = u2h(q.z); tmp[4 * i + 3] = u2h(q.w);
           }
+        } else if constexpr (W % 4 == 0) {
+#pragma unroll
+          for (int i = 0; i < W / 4; ++i) {
+            const uint2 q = *reinterpret_cast<const uint2*>(s + 8 * i);
+            tmp[2 * i] = u2h(q.x); tmp[2 * i + 1] = u2h(q.y);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < W / 2; ++i) tmp[i] = u2h(*reinterpret_cast<const uint32_t*>(s + 4 * i));
         }
 #pragma unroll
         for (int i = 0; i < W / 2; ++i) {
@@ -189,15 +199,18 @@ __device__ __forceinline__ void rload(const unsigned char* s, Row<CP, W>& r) {
     }
   } else if constexpr (SP == P32) {
     const float* fp = reinterpret_cast<const float*>(s);
-    if constexpr (W >= 4) {
+    if constexpr (W % 4 == 0) {
 #pragma unroll
       for (int i = 0; i < W / 4; ++i) {
         const float4 q = *reinterpret_cast<const float4*>(fp + 4 * i);
         r.v[4 * i] = q.x; r.v[4 * i + 1] = q.y; r.v[4 * i + 2] = q.z; r.v[4 * i + 3] = q.w;
       }
-    } else if constexpr (W == 2) {
-      const float2 q = *reinterpret_cast<const float2*>(fp);
-      r.v[0] = q.x; r.v[1] = q.y;
+    } else if constexpr (W % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < W / 2; ++i) {
+        const float2 q = *reinterpret_cast<const float2*>(fp + 2 * i);
+        r.v[2 * i] = q.x; r.v[2 * i + 1] = q.y;
+      }
     } else {
       r.v[0] = fp[0];
     }
@@ -319,22 +332,28 @@ __device__ __forceinline__ void gstore(void* base, long long idx, const Row<SP, 
   if constexpr (SP == P16) {
     __half* p = static_cast<__half*>(base) + idx;
     if constexpr (W == 1) *p = r.h;
-    else if constexpr (W == 2) *reinterpret_cast<uint32_t*>(p) = h2u(r.h[0]);
-    else if constexpr (W == 4) *reinterpret_cast<uint2*>(p) = make_uint2(h2u(r.h[0]), h2u(r.h[1]));
-    else {
+    else if constexpr (W % 8 == 0) {
 #pragma unroll
       for (int i = 0; i < W / 8; ++i)
         reinterpret_cast<uint4*>(p)[i] =
             make_uint4(h2u(r.h[4 * i]), h2u(r.h[4 * i + 1]), h2u(r.h[4 * i + 2]), h2u(r.h[4 * i + 3]));
+    } else if constexpr (W % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < W / 4; ++i) reinterpret_cast<uint2*>(p)[i] = make_uint2(h2u(r.h[2 * i]), h2u(r.h[2 * i + 1]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < W / 2; ++i) reinterpret_cast<uint32_t*>(p)[i] = h2u(r.h[i]);
     }
   } else if constexpr (SP == P32) {
     float* p = static_cast<float*>(base) + idx;
-    if constexpr (W >= 4) {
+    if constexpr (W % 4 == 0) {
 #pragma unroll
       for (int i = 0; i < W / 4; ++i)
         reinterpret_cast<float4*>(p)[i] = make_float4(r.v[4 * i], r.v[4 * i + 1], r.v[4 * i + 2], r.v[4 * i + 3]);
-    } else if constexpr (W == 2) *reinterpret_cast<float2*>(p) = make_float2(r.v[0], r.v[1]);
-    else *p = r.v[0];
+    } else if constexpr (W % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < W / 2; ++i) reinterpret_cast<float2*>(p)[i] = make_float2(r.v[2 * i], r.v[2 * i + 1]);
+    } else *p = r.v[0];
   } else {
     double* p = static_cast<double*>(base) + idx;
     if constexpr (W >= 2) {
@@ -350,28 +369,36 @@ __device__ __forceinline__ void gload(const void* base, long long idx, Row<SP, W
   if constexpr (SP == P16) {
     const __half* p = static_cast<const __half*>(base) + idx;
     if constexpr (W == 1) r.h = __ldg(p);
-    else if constexpr (W == 2) r.h[0] = u2h(__ldg(reinterpret_cast<const unsigned int*>(p)));
-    else if constexpr (W == 4) {
-      const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
-      r.h[0] = u2h(q.x); r.h[1] = u2h(q.y);
-    } else {
+    else if constexpr (W % 8 == 0) {
 #pragma unroll
       for (int i = 0; i < W / 8; ++i) {
         const uint4 q = __ldg(reinterpret_cast<const uint4*>(p) + i);
         r.h[4 * i] = u2h(q.x); r.h[4 * i + 1] = u2h(q.y); r.h[4 * i + 2] = u2h(q.z); r.h[4 * i + 3] = u2h(q.w);
       }
+    } else if constexpr (W % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < W / 4; ++i) {
+        const uint2 q = __ldg(reinterpret_cast<const uint2*>(p) + i);
+        r.h[2 * i] = u2h(q.x); r.h[2 * i + 1] = u2h(q.y);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < W / 2; ++i) r.h[i] = u2h(__ldg(reinterpret_cast<const unsigned int*>(p) + i));
     }
   } else if constexpr (SP == P32) {
     const float* p = static_cast<const float*>(base) + idx;
-    if constexpr (W >= 4) {
+    if constexpr (W % 4 == 0) {
 #pragma unroll
       for (int i = 0; i < W / 4; ++i) {
         const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i);
         r.v[4 * i] = q.x; r.v[4 * i + 1] = q.y; r.v[4 * i + 2] = q.z; r.v[4 * i + 3] = q.w;
       }
-    } else if constexpr (W == 2) {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(p));
-      r.v[0] = q.x; r.v[1] = q.y;
+    } else if constexpr (W % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < W / 2; ++i) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(p) + i);
+        r.v[2 * i] = q.x; r.v[2 * i + 1] = q.y;
+      }
     } else r.v[0] = __ldg(p);
   } else {
     const double* p = static_cast<const double*>(base) + idx;

@@ -20,7 +20,8 @@ using namespace mpmg_dev;
 // Jacobi only)
 template <int LP, int CP, int OP, int P, int V = 0>
 struct PlaneCfg {
-  static constexpr int W = (V == 10 && P >= 128) ? 4 : (P >= 256 ? 8 : P / 32);
+  // (P = 192, the finest pitch of the paper's 193^3 grid: W = 6 everywhere)
+  static constexpr int W = (V == 10 && P >= 128 && (P / 32) % 4 == 0) ? 4 : (P >= 256 ? 8 : P / 32);
   static constexpr int WX = P / (32 * W);
   static constexpr bool kWide = CP == P64 || (CP == P32 && LP != P16) || OP == POP_UPDATE || OP == POP_UPDATE_R;
   // output rows per thread and warp-rows per CTA
@@ -217,6 +218,7 @@ inline bool with_pitch(int P, F&& f) {
     case 32: f(std::integral_constant<int, 32>{}); return true;
     case 64: f(std::integral_constant<int, 64>{}); return true;
     case 128: f(std::integral_constant<int, 128>{}); return true;
+    case 192: f(std::integral_constant<int, 192>{}); return true;
     case 256: f(std::integral_constant<int, 256>{}); return true;
     case 512: f(std::integral_constant<int, 512>{}); return true;
     case 1024: f(std::integral_constant<int, 1024>{}); return true;
