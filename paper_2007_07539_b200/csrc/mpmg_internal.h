@@ -103,6 +103,9 @@ bool plane_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* 
                     double* partials, void* ring, long long ring_len, const int* slot, double* ring_scale, bool fma,
                     cudaStream_t s, cudaError_t* err, const mpmg_slab* slab = nullptr);
 int plane_update_r_partials(int dim, int nodes, int lp, int pz = 0);
+bool stencil_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* r, const double* alpha_dev,
+                      double* partials, void* ring, long long ring_len, const int* slot, double* ring_scale, bool fma,
+                      cudaStream_t s, cudaError_t* err);
 // true when the streaming stencil kernels support this level shape
 bool stencil_supported(int dim, int nodes, int prec);
 

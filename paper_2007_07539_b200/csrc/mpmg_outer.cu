@@ -48,6 +48,34 @@ cudaError_t launch_update_rc(const mpmg_stencil& A64, const void* c, int c_prec,
   return A64.dim == 3 ? by_fma(I3{}) : by_fma(I2{});
 }
 
+// r -= a A c (+ partials) and c into ring slot *slot: the streaming form of
+// plane_update_r for shapes the plane kernels do not take (2D levels, pitches
+// that are not a power of two); binary16/32 c only
+bool stencil_update_r(const mpmg_stencil& A64, const void* c, int c_prec, double* r, const double* alpha_dev,
+                      double* partials, void* ring, long long ring_len, const int* slot, double* ring_scale, bool fma,
+                      cudaStream_t s, cudaError_t* err) {
+  if (c_prec == MPMG_FP64) return false;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  auto go = [&](auto dimc, auto lpc, auto fmc) -> cudaError_t {
+    constexpr int D = decltype(dimc)::value, L = decltype(lpc)::value;
+    constexpr bool M = decltype(fmc)::value;
+    StencilArgs a = make_args(A64, Geo<L, P64>::ZC);
+    a.x = c; a.r64 = r; a.alpha = alpha_dev; a.partials = partials;
+    a.ring = ring; a.ring_len = ring_len; a.ring_slot = slot; a.ring_scale = ring_scale;
+    return run_stencil<D, L, P64, P64, OP_UPDATE_R, false, M>(a, s);
+  };
+  auto by_prec = [&](auto dimc, auto fmc) -> cudaError_t {
+    return c_prec == MPMG_FP16 ? go(dimc, std::integral_constant<int, P16>{}, fmc)
+                               : go(dimc, std::integral_constant<int, P32>{}, fmc);
+  };
+  auto by_fma = [&](auto dimc) -> cudaError_t {
+    return fma ? by_prec(dimc, std::true_type{}) : by_prec(dimc, std::false_type{});
+  };
+  *err = A64.dim == 3 ? by_fma(I3{}) : by_fma(I2{});
+  return true;
+}
+
 // partial sums written by the FP64-epilogue kernels (update: stencil operand
 // in precision lp; defect64/resnorm: lp == FP64)
 int stencil_partials(int dim, int nodes, int lp, bool update) {

@@ -324,7 +324,9 @@ struct mpmg_solver {
     ring_cycle = false;
     if (ring_k > 0) {  // ir_solver.cpp:112, the u half deferred
       if (e == cudaSuccess && !plane_update_r(A64, c, fp, r, &st->scale, partU, ring, ring_len, &st->pending,
-                                              ring_scale, fma(), q, &e))
+                                              ring_scale, fma(), q, &e) &&
+          !stencil_update_r(A64, c, fp, r, &st->scale, partU, ring, ring_len, &st->pending, ring_scale, fma(), q,
+                            &e))
         e = cudaErrorInvalidValue;
       if (e == cudaSuccess)
         e = launch_fold(len, u, ring, ring_len, fp, ring_scale, &st->pending, 1, &st->fold_now, fma(), q, &st->u_zero);
@@ -542,7 +544,9 @@ mpmg_solver* mpmg_solver_create(const mpmg_solver_config* cfg, int* err, int* er
   S->nU = stencil_partials(c.dim, c.nodes, fprec, true);
   S->nD = stencil_partials(c.dim, c.nodes, MPMG_FP64, false);
   if (env_ll("MPMG_DEFER_U", 1) != 0 && fprec != MPMG_FP64) {
-    const int nr = plane_update_r_partials(c.dim, c.nodes, fprec);
+    int nr = plane_update_r_partials(c.dim, c.nodes, fprec);
+    if (nr <= 0 && stencil_supported(c.dim, c.nodes, fprec))  // the streaming UPDATE_R (2D, other pitches)
+      nr = stencil_partials(c.dim, c.nodes, fprec, true);
     if (nr > 0) {
       S->ring_k = 10;
       S->nU = nr;

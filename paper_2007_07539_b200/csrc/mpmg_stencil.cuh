@@ -31,7 +31,10 @@
 
 namespace mpmg_dev {
 
-enum { OP_SPMV = 0, OP_DEFECT = 1, OP_JACOBI = 2, OP_DEFECT64 = 3, OP_RESNORM = 4, OP_UPDATE = 5 };
+enum { OP_SPMV = 0, OP_DEFECT = 1, OP_JACOBI = 2, OP_DEFECT64 = 3, OP_RESNORM = 4, OP_UPDATE = 5, OP_UPDATE_R = 6 };
+// OP_UPDATE_R: the r half of OP_UPDATE (r -= a A c, + partials) and c copied
+//   into ring slot *ring_slot (deferred u += a c, as POP_UPDATE_R in
+//   mpmg_plane.cuh; the streaming form serves 2D and non-plane pitches)
 
 struct StencilArgs {
   int P;             // pitch (nodes - 1)
@@ -51,6 +54,10 @@ struct StencilArgs {
   const double* alpha;  // OP_UPDATE scale (device scalar)
   double* partials;  // optional per-block sum of squares
   const int* gate;   // optional device flag: kernel is a no-op unless *gate != 0
+  void* ring;          // OP_UPDATE_R: correction ring (slots of ring_len values, precision LP)
+  long long ring_len;
+  const int* ring_slot;
+  double* ring_scale;  // per-slot scale (= *alpha)
 };
 
 template <int CP> struct Taps;
@@ -60,7 +67,7 @@ template <> struct Taps<P64> { static __device__ __forceinline__ double get(cons
 
 template <int OP> struct OpTraits {
   static constexpr bool kNeedB = OP == OP_DEFECT || OP == OP_JACOBI || OP == OP_DEFECT64 || OP == OP_RESNORM;
-  static constexpr bool kNorm = OP == OP_DEFECT64 || OP == OP_RESNORM || OP == OP_UPDATE;
+  static constexpr bool kNorm = OP == OP_DEFECT64 || OP == OP_RESNORM || OP == OP_UPDATE || OP == OP_UPDATE_R;
 };
 
 // block-level deterministic sum of one double per thread -> partials[block]
@@ -90,6 +97,10 @@ __global__ void __launch_bounds__(32 * BW) k_stencil(const __grid_constant__ Ste
   using S = typename Scalar<CP>::T;
 
   if (a.gate && *a.gate == 0) return;  // uniform across the grid
+  if constexpr (OP == OP_UPDATE_R) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+      a.ring_scale[*a.ring_slot] = *a.alpha;
+  }
   const int lane = threadIdx.x;
   const int P = a.P;
   const long long xchunk = DIM == 3 ? (long long)blockIdx.x * 32 + lane
@@ -148,6 +159,7 @@ __global__ void __launch_bounds__(32 * BW) k_stencil(const __grid_constant__ Ste
           uo[i] = vload_rw<P64, W>(a.u64, idx, v);
           ro[i] = vload_rw<P64, W>(a.r64, idx, v);
         }
+        if constexpr (OP == OP_UPDATE_R) ro[i] = vload_rw<P64, W>(a.r64, idx, v);
       }
     }
 
@@ -238,6 +250,21 @@ __global__ void __launch_bounds__(32 * BW) k_stencil(const __grid_constant__ Ste
             vstore<P64, W>(a.u64, idx, un);
             vstore<P64, W>(a.r64, idx, rn);
             sq = vsumsq<P64, W>(rn, sq);
+          }
+        } else if constexpr (OP == OP_UPDATE_R) {
+          const double al = *a.alpha;
+          Vec<P64, W> rn;
+#pragma unroll
+          for (int k = 0; k < W; ++k) rn.v[k] = fma64<FMA>(-al, t.v[k], ro[i].v[k]);
+          if (x0 == 0) vzero_first<P64, W>(rn);
+          if (v) {
+            vstore<P64, W>(a.r64, idx, rn);
+            sq = vsumsq<P64, W>(rn, sq);
+            // c unchanged into the ring slot (its x = 0 ghost is zero)
+            const Vec<LP, W> craw = vload_rw<LP, W>(a.x, idx, true);
+            vstore<LP, W>(static_cast<unsigned char*>(a.ring) +
+                              (long long)*a.ring_slot * a.ring_len * (LP == P16 ? 2 : (LP == P32 ? 4 : 8)),
+                          idx, craw);
           }
         }
       }

@@ -201,11 +201,12 @@ def test_scaling_forced_off_stagnates_h_mg():
     ("h_mg", 10, 14, 1e-30),    # fold at 10, 4 parked corrections folded after the loop
 ])
 @pytest.mark.parametrize("graph", [True, False])
-def test_deferred_corrections_bitwise(variant, refresh, max_it, tol, graph, monkeypatch):
+@pytest.mark.parametrize("dim,n,L", [(3, 65, 6), (2, 257, 8), (3, 97, 6)])
+def test_deferred_corrections_bitwise(variant, refresh, max_it, tol, graph, dim, n, L, monkeypatch):
     """The deferred u += a c (ring of parked corrections, mpmg_solver.cu) gives
     the bitwise solution, residual history and iteration count of the fused
-    per-iteration update_residuum_correction (kernels.cpp:300-341)."""
-    dim, n, L = 3, 65, 6
+    per-iteration update_residuum_correction (kernels.cpp:300-341) -- with the
+    plane UPDATE_R (3D 65^3) and the streaming one (2D; pitch 96)."""
     b = mg.problem_rhs(dim, n)
     out = []
     for defer in ("1", "0"):
