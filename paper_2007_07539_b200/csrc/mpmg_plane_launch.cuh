@@ -46,6 +46,16 @@ inline int plane_variant() {
   return v;
 }
 
+inline int plane_variant128() {  // the same shapes for the pitch-128 Jacobi (MPMG_PLANE_VARIANT128)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MPMG_PLANE_VARIANT128");
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 5) v = 0;
+  }
+  return v;
+}
+
 inline int outer_waves() {
   static int v = -1;
   if (v < 0) {
@@ -341,9 +351,10 @@ bool plane_level_op(int op, const mpmg_stencil& A, const void* x, const void* b,
     else if (op == 3) *err = ftz ? PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, true, true, PP>::run(a, s)
                                  : PlaneLaunch<LP, LP, LP, POP_JACOBI_Z, false, true, PP>::run(a, s);
     else {
-      if constexpr (LP == P16 && PP == 256) {  // tuning shapes (MPMG_PLANE_VARIANT)
-        if (!ftz && plane_variant() > 0) {
-          switch (plane_variant()) {
+      if constexpr (LP == P16 && (PP == 256 || PP == 128)) {  // tuning shapes (MPMG_PLANE_VARIANT[128])
+        const int pv = PP == 256 ? plane_variant() : plane_variant128();
+        if (!ftz && pv > 0) {
+          switch (pv) {
             case 1: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 1>::run(a, s); break;
             case 2: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 2>::run(a, s); break;
             case 3: *err = PlaneLaunch<LP, LP, LP, POP_JACOBI, false, true, PP, 3>::run(a, s); break;
