@@ -690,6 +690,11 @@ def run_dist(a):
     mg._check(lib.mpmg_dev_d2h(uh.data_ptr(), uptr, uh.numel() * 8), "d2h")
     te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=tdev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # kernels this rank launched in the timed solves: the captured graph's
+    # kernel nodes (init + final, and one IR iteration per WHILE pass)
+    gk = d.graph_kernels()
+    per_solve = gk[0] + rep.iterations * gk[1] if gk else None
+    launches = per_solve * a.steps if per_solve is not None else None
     if rank == 0:
         N = mg.unknowns(dim, n)
         out = {"metric": METRIC, "value": float(t.item()), "unit": UNIT, "n_gpus": ws, "steps": a.steps,
@@ -708,7 +713,8 @@ def run_dist(a):
                "tolerance": tol, "rhs_assembly_s": rhs_s, "clocks": clocks,
                "e2e": {"value": float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(slab.nbytes * ws),
                        "d2h_bytes_per_step": int(slab.nbytes * ws), "path": "mpmg_dist_solve_device (C ABI), slabs"},
-               "gpu_launches": None}
+               "gpu_launches": launches,
+               "gpu_launches_per_solve": {"rank0": per_solve, "graph_kernels_outer_per_iteration": gk}}
         print(json.dumps(out), flush=True)
     dist.barrier()
     d.close()

@@ -397,6 +397,10 @@ int mpmg_dist_buffers(mpmg_dist* d, double** b_slab, double** u_slab);
  * those done as kernel + peer copy (MPMG_DIST_FUSE_HALOS=0, or levels the
  * fused kernel does not cover: pitch <= 64, FP64 u, agglomeration) */
 int mpmg_dist_exchange_stats(const mpmg_dist* d, int32_t* fused, int32_t* copied);
+/* kernel launches of the captured solve graph: init + final (outer) and one
+ * IR iteration (the WHILE body); a solve of k iterations launches
+ * outer + k * per_iteration kernels. MPMG_EINVAL before the graph exists. */
+int mpmg_dist_graph_kernels(const mpmg_dist* d, int32_t* outer, int32_t* per_iteration);
 void* mpmg_dist_stream(mpmg_dist* d);
 /* the agglomeration level's replicated rhs / correction (full padded vectors
  * in that level's precision), after a solve: the last cycle's */

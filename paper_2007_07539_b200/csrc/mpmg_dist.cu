@@ -210,6 +210,7 @@ struct mpmg_dist {
   bool fuse_halos = true;         // MPMG_DIST_FUSE_HALOS=0: kernel + copy exchange
   bool fuse_jz = true;            // MPMG_DIST_JZ=0: pointwise step 1 + stencil step 2
   int n_fused = 0, n_copied = 0;  // halo exchanges recorded in the last graph
+  int n_kern_outer = -1, n_kern_body = -1;  // its kernel nodes: init + final, one iteration
 
   template <typename T = void>
   T* at(size_t off) { return reinterpret_cast<T*>(arena + off); }
@@ -515,7 +516,22 @@ struct mpmg_dist {
     return e;
   }
 
+  // kernel nodes of a captured graph (top level: the WHILE node's body counted apart)
+  static int kernel_nodes(cudaGraph_t gr) {
+    size_t n = 0;
+    if (cudaGraphGetNodes(gr, nullptr, &n) != cudaSuccess) { cudaGetLastError(); return -1; }
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (n && cudaGraphGetNodes(gr, nodes.data(), &n) != cudaSuccess) { cudaGetLastError(); return -1; }
+    int k = 0;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+  }
+
   cudaError_t build_graph(const mpmg_solve_params& p) {
+    n_kern_outer = n_kern_body = -1;
     if (exec) { cudaGraphExecDestroy(exec); exec = nullptr; }
     gvalid = false;
     n_fused = n_copied = 0;
@@ -553,6 +569,7 @@ struct mpmg_dist {
           cudaGraph_t dummy = nullptr;
           const cudaError_t e3 = cudaStreamEndCapture(body_s, &dummy);
           e = e2 != cudaSuccess ? e2 : e3;
+          if (e == cudaSuccess) n_kern_body = kernel_nodes(body);
         }
       }
       if (e == cudaSuccess) e = enqueue_final(s);
@@ -560,6 +577,7 @@ struct mpmg_dist {
       const cudaError_t e4 = cudaStreamEndCapture(s, &out);
       if (e == cudaSuccess) e = e4;
       g = e4 == cudaSuccess ? out : nullptr;
+      if (g) n_kern_outer = kernel_nodes(g);
     }
     cudaStreamDestroy(body_s);
     if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
@@ -771,6 +789,13 @@ int mpmg_dist_exchange_stats(const mpmg_dist* D, int32_t* fused, int32_t* copied
   if (!D) return MPMG_EINVAL;
   if (fused) *fused = D->n_fused;
   if (copied) *copied = D->n_copied;
+  return MPMG_OK;
+}
+
+int mpmg_dist_graph_kernels(const mpmg_dist* D, int32_t* outer, int32_t* per_iteration) {
+  if (!D || D->n_kern_outer < 0 || D->n_kern_body < 0) return MPMG_EINVAL;
+  if (outer) *outer = D->n_kern_outer;
+  if (per_iteration) *per_iteration = D->n_kern_body;
   return MPMG_OK;
 }
 

@@ -489,6 +489,8 @@ class DistSolver:
         L.mpmg_dist_stream.restype = vp; L.mpmg_dist_stream.argtypes = [vp]
         L.mpmg_dist_exchange_stats.restype = C.c_int
         L.mpmg_dist_exchange_stats.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+        L.mpmg_dist_graph_kernels.restype = C.c_int
+        L.mpmg_dist_graph_kernels.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
         from . import SolveParams, SolveReportC
         L.mpmg_dist_prepare.restype = C.c_int
         L.mpmg_dist_prepare.argtypes = [vp, C.POINTER(SolveParams)]
@@ -527,6 +529,13 @@ class DistSolver:
         f, c = C.c_int32(), C.c_int32()
         self.L.mpmg_dist_exchange_stats(self.h, C.byref(f), C.byref(c))
         return f.value, c.value
+
+    def graph_kernels(self):
+        """(outer, per_iteration): kernel nodes of the captured solve graph;
+        a solve of k iterations launches outer + k * per_iteration kernels"""
+        o, b = C.c_int32(), C.c_int32()
+        rc = self.L.mpmg_dist_graph_kernels(self.h, C.byref(o), C.byref(b))
+        return (o.value, b.value) if rc == 0 else None
 
     def buffers(self):
         b, u = C.c_void_p(), C.c_void_p()
